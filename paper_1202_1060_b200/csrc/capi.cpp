@@ -1,0 +1,634 @@
+// capi.cpp -- the extern "C" boundary (include/ldpc_b200.h): handles,
+// validation, error mapping, device uploads and stream orchestration.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+
+#include "host.hpp"
+#include "kernels.cuh"
+#include "rng.cuh"
+#include "ldpc_b200.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct CudaFailure : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaFailure(std::string(what) + ": " + cudaGetErrorString(e));
+}
+void cuda_check(int e, const char* what) { cuda_check(static_cast<cudaError_t>(e), what); }
+
+template <class F>
+int guard(F&& f) {
+  try {
+    g_last_error.clear();
+    return f();
+  } catch (const ldpcb::AlistFailure& e) {
+    g_last_error = e.what();
+    return LDPCB_EALIST;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return LDPCB_EINVAL;
+  } catch (const CudaFailure& e) {
+    g_last_error = e.what();
+    return LDPCB_ECUDA;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return LDPCB_ERUNTIME;
+  }
+}
+
+template <class T>
+T* upload(const std::vector<T>& v) {
+  T* d = nullptr;
+  const size_t bytes = std::max<size_t>(1, v.size()) * sizeof(T);
+  cuda_check(cudaMalloc(&d, bytes), "cudaMalloc");
+  if (!v.empty()) cuda_check(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "cudaMemcpy");
+  return d;
+}
+
+struct DevArrays {
+  std::vector<void*> ptrs;
+  ~DevArrays() {}
+};
+
+void free_on(int dev, std::vector<void*>& ptrs) {
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess) return;
+  cudaSetDevice(dev);
+  for (void* p : ptrs) cudaFree(p);
+  cudaSetDevice(cur);
+  ptrs.clear();
+}
+
+struct CodeImpl {
+  ldpcb::CodeData host;
+  bool cregular = true, vregular = true;
+  std::mutex mu;
+  struct Dev {
+    int32_t *row_off, *cols, *var_off, *var_edges;
+    std::vector<void*> ptrs;
+  };
+  std::map<int, Dev> dev;
+
+  explicit CodeImpl(ldpcb::CodeData c) : host(std::move(c)) {
+    for (int r = 0; r < host.m; ++r) cregular &= (host.row_off[r + 1] - host.row_off[r]) == host.max_cdeg;
+    for (int v = 0; v < host.n; ++v) vregular &= (host.var_off[v + 1] - host.var_off[v]) == host.max_vdeg;
+  }
+  ~CodeImpl() {
+    for (auto& kv : dev) free_on(kv.first, kv.second.ptrs);
+  }
+  const Dev& device() {
+    int d = 0;
+    cuda_check(cudaGetDevice(&d), "cudaGetDevice");
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = dev.find(d);
+    if (it != dev.end()) return it->second;
+    Dev x;
+    x.row_off = upload(host.row_off);
+    x.cols = upload(host.cols);
+    x.var_off = upload(host.var_off);
+    x.var_edges = upload(host.var_edges);
+    x.ptrs = {x.row_off, x.cols, x.var_off, x.var_edges};
+    return dev.emplace(d, std::move(x)).first->second;
+  }
+};
+
+struct SchedImpl {
+  std::shared_ptr<CodeImpl> code;
+  ldpcb::ScheduleData host;
+  std::mutex mu;
+  struct Dev {
+    int32_t *grp_off, *grp_cns, *touch_off, *touch_vns;
+    std::vector<void*> ptrs;
+  };
+  std::map<int, Dev> dev;
+
+  ~SchedImpl() {
+    for (auto& kv : dev) free_on(kv.first, kv.second.ptrs);
+  }
+  const Dev& device() {
+    int d = 0;
+    cuda_check(cudaGetDevice(&d), "cudaGetDevice");
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = dev.find(d);
+    if (it != dev.end()) return it->second;
+    Dev x;
+    x.grp_off = upload(host.grp_off);
+    x.grp_cns = upload(host.grp_cns);
+    x.touch_off = upload(host.touch_off);
+    x.touch_vns = upload(host.touch_vns);
+    x.ptrs = {x.grp_off, x.grp_cns, x.touch_off, x.touch_vns};
+    return dev.emplace(d, std::move(x)).first->second;
+  }
+};
+
+}  // namespace
+
+struct ldpcb_code_s {
+  std::shared_ptr<CodeImpl> impl;
+};
+struct ldpcb_schedule_s {
+  std::shared_ptr<SchedImpl> impl;
+};
+
+namespace {
+
+void need(bool ok, const char* msg) {
+  if (!ok) throw std::invalid_argument(msg);
+}
+
+int make_code(ldpcb::CodeData c, ldpcb_code* out) {
+  need(out != nullptr, "null output handle");
+  *out = new ldpcb_code_s{std::make_shared<CodeImpl>(std::move(c))};
+  return LDPCB_OK;
+}
+
+int make_sched(const std::shared_ptr<CodeImpl>& code, ldpcb::ScheduleData s, ldpcb_schedule* out) {
+  need(out != nullptr, "null output handle");
+  auto impl = std::make_shared<SchedImpl>();
+  impl->code = code;
+  impl->host = std::move(s);
+  *out = new ldpcb_schedule_s{impl};
+  return LDPCB_OK;
+}
+
+ldpcb::DevGraph dev_graph(ldpcb_code code, ldpcb_schedule s) {
+  need(code && s, "null handle");
+  need(s->impl->code.get() == code->impl.get(), "schedule was built for a different code");
+  const auto& c = code->impl->device();
+  const auto& d = s->impl->device();
+  const auto& h = code->impl->host;
+  ldpcb::DevGraph g;
+  g.n = h.n;
+  g.m = h.m;
+  g.E = h.E;
+  g.G = s->impl->host.G;
+  g.max_cdeg = h.max_cdeg;
+  g.max_vdeg = h.max_vdeg;
+  g.cregular = code->impl->cregular;
+  g.vregular = code->impl->vregular;
+  g.row_off = c.row_off;
+  g.cols = c.cols;
+  g.var_off = c.var_off;
+  g.var_edges = c.var_edges;
+  g.grp_off = d.grp_off;
+  g.grp_cns = d.grp_cns;
+  g.touch_off = d.touch_off;
+  g.touch_vns = d.touch_vns;
+  return g;
+}
+
+ldpcb::Rows rows_from_csr(int m, const int32_t* off, const int32_t* cols) {
+  need(off != nullptr && cols != nullptr, "null CSR arrays");
+  need(off[0] == 0, "row offsets must start at 0");
+  ldpcb::Rows rows(m);
+  for (int r = 0; r < m; ++r) {
+    need(off[r + 1] >= off[r], "row offsets must be non-decreasing");
+    rows[r].assign(cols + off[r], cols + off[r + 1]);
+  }
+  return rows;
+}
+
+void launch(int err, const char* what) { cuda_check(err, what); }
+
+}  // namespace
+
+extern "C" {
+
+const char* ldpcb_last_error(void) { return g_last_error.c_str(); }
+int ldpcb_abi_version(void) { return 1; }
+
+int ldpcb_code_from_check_lists(int n_vars, int n_checks, const int32_t* row_off, const int32_t* cols,
+                                ldpcb_code* out) {
+  return guard([&] {
+    need(n_checks >= 1 && n_vars >= 1, "graph must have at least one VN and one CN");
+    return make_code(ldpcb::build_code(n_vars, rows_from_csr(n_checks, row_off, cols)), out);
+  });
+}
+
+int ldpcb_code_random_regular(int n_vars, int dv, int dc, uint64_t seed, ldpcb_code* out) {
+  return guard([&] { return make_code(ldpcb::build_code(n_vars, ldpcb::regular_rows(n_vars, dv, dc, seed)), out); });
+}
+
+int ldpcb_code_random_regular_girth6(int n_vars, int dv, int dc, uint64_t seed, ldpcb_code* out) {
+  return guard([&] {
+    auto rows = ldpcb::regular_rows(n_vars, dv, dc, seed);
+    ldpcb::break_4cycles(n_vars, rows, seed);
+    return make_code(ldpcb::build_code(n_vars, rows), out);
+  });
+}
+
+int ldpcb_code_qc(int base_rows, int base_cols, int z, double p_empty, int min_col_degree, uint64_t seed,
+                  ldpcb_code* out) {
+  return guard([&] {
+    auto rows = ldpcb::qc_rows(base_rows, base_cols, z, p_empty, min_col_degree, seed);
+    return make_code(ldpcb::build_code(base_cols * z, rows), out);
+  });
+}
+
+int ldpcb_code_irregular(int n_vars, int n_classes, const int32_t* vn_degrees, const int32_t* vn_counts, int dc,
+                         uint64_t seed, ldpcb_code* out) {
+  return guard([&] {
+    need(n_classes >= 1 && vn_degrees && vn_counts, "need at least one degree class");
+    std::vector<int> d(vn_degrees, vn_degrees + n_classes), c(vn_counts, vn_counts + n_classes);
+    return make_code(ldpcb::build_code(n_vars, ldpcb::irregular_rows(n_vars, d, c, dc, seed)), out);
+  });
+}
+
+int ldpcb_code_parse_alist(const char* text, ldpcb_code* out, int* err_kind, int* err_line) {
+  return guard([&] {
+    need(text != nullptr, "null text");
+    try {
+      return make_code(ldpcb::parse_alist(text), out);
+    } catch (const ldpcb::AlistFailure& e) {
+      if (err_kind) *err_kind = static_cast<int>(e.kind);
+      if (err_line) *err_line = e.line;
+      throw;
+    }
+  });
+}
+
+int ldpcb_code_serialize_alist(ldpcb_code code, char* buf, int64_t cap, int64_t* len) {
+  return guard([&] {
+    need(code != nullptr, "null handle");
+    const std::string s = ldpcb::serialize_alist(code->impl->host);
+    if (len) *len = static_cast<int64_t>(s.size());
+    if (buf && cap > static_cast<int64_t>(s.size())) std::memcpy(buf, s.c_str(), s.size() + 1);
+    return LDPCB_OK;
+  });
+}
+
+int ldpcb_code_dims(ldpcb_code code, int32_t* n_vars, int32_t* n_checks, int32_t* n_edges, int32_t* max_cdeg,
+                    int32_t* max_vdeg) {
+  return guard([&] {
+    need(code != nullptr, "null handle");
+    const auto& h = code->impl->host;
+    if (n_vars) *n_vars = h.n;
+    if (n_checks) *n_checks = h.m;
+    if (n_edges) *n_edges = h.E;
+    if (max_cdeg) *max_cdeg = h.max_cdeg;
+    if (max_vdeg) *max_vdeg = h.max_vdeg;
+    return LDPCB_OK;
+  });
+}
+
+int ldpcb_code_export(ldpcb_code code, int32_t* row_off, int32_t* cols, int32_t* var_off, int32_t* var_cns,
+                      int32_t* var_edges) {
+  return guard([&] {
+    need(code != nullptr, "null handle");
+    const auto& h = code->impl->host;
+    auto put = [](int32_t* dst, const std::vector<int32_t>& v) {
+      if (dst) std::memcpy(dst, v.data(), v.size() * sizeof(int32_t));
+    };
+    put(row_off, h.row_off);
+    put(cols, h.cols);
+    put(var_off, h.var_off);
+    put(var_cns, h.var_cns);
+    put(var_edges, h.var_edges);
+    return LDPCB_OK;
+  });
+}
+
+int ldpcb_code_count_4cycles(ldpcb_code code, int64_t* count) {
+  return guard([&] {
+    need(code != nullptr && count != nullptr, "null argument");
+    *count = ldpcb::count_4cycles(code->impl->host);
+    return LDPCB_OK;
+  });
+}
+
+void ldpcb_code_destroy(ldpcb_code code) { delete code; }
+
+int ldpcb_schedule_from_groups(ldpcb_code code, int kind, int n_groups, const int32_t* grp_off,
+                               const int32_t* grp_cns, ldpcb_schedule* out) {
+  return guard([&] {
+    need(code != nullptr, "null handle");
+    need(kind >= 0 && kind <= 2, "unknown schedule kind");
+    need(n_groups >= 1, "schedule needs at least one group");
+    auto groups = rows_from_csr(n_groups, grp_off, grp_cns);
+    return make_sched(code->impl,
+                      ldpcb::schedule_from_groups(code->impl->host, static_cast<ldpcb::Kind>(kind), groups), out);
+  });
+}
+
+int ldpcb_schedule_flooding(ldpcb_code code, ldpcb_schedule* out) {
+  return guard([&] {
+    need(code != nullptr, "null handle");
+    return make_sched(code->impl, ldpcb::flooding_schedule(code->impl->host), out);
+  });
+}
+
+int ldpcb_schedule_disjoint(ldpcb_code code, int n_groups, uint64_t seed, ldpcb_schedule* out) {
+  return guard([&] {
+    need(code != nullptr, "null handle");
+    return make_sched(code->impl,
+                      ldpcb::reference_random_schedule(code->impl->host, ldpcb::Kind::disjoint, n_groups, 0.0, seed),
+                      out);
+  });
+}
+
+int ldpcb_schedule_nondisjoint(ldpcb_code code, int n_groups, double overlap, uint64_t seed, ldpcb_schedule* out) {
+  return guard([&] {
+    need(code != nullptr, "null handle");
+    return make_sched(
+        code->impl,
+        ldpcb::reference_random_schedule(code->impl->host, ldpcb::Kind::nondisjoint, n_groups, overlap, seed), out);
+  });
+}
+
+int ldpcb_schedule_windows(ldpcb_code code, int kind, int n_groups, int window, int stride, ldpcb_schedule* out) {
+  return guard([&] {
+    need(code != nullptr, "null handle");
+    need(kind >= 0 && kind <= 2, "unknown schedule kind");
+    return make_sched(code->impl,
+                      ldpcb::window_schedule(code->impl->host, static_cast<ldpcb::Kind>(kind), n_groups, window,
+                                             stride),
+                      out);
+  });
+}
+
+int ldpcb_schedule_dims(ldpcb_schedule s, int32_t* kind, int32_t* n_groups, int32_t* n_slots, int32_t* group_size,
+                        double* overlap, int64_t* edge_updates_per_iter, int64_t* touched_per_iter) {
+  return guard([&] {
+    need(s != nullptr, "null handle");
+    const auto& h = s->impl->host;
+    if (kind) *kind = static_cast<int32_t>(h.kind);
+    if (n_groups) *n_groups = h.G;
+    if (n_slots) *n_slots = static_cast<int32_t>(h.grp_cns.size());
+    if (group_size) *group_size = h.group_size;
+    if (overlap) *overlap = h.overlap;
+    if (edge_updates_per_iter) *edge_updates_per_iter = h.edge_updates_per_iter;
+    if (touched_per_iter) *touched_per_iter = h.touched_per_iter;
+    return LDPCB_OK;
+  });
+}
+
+int ldpcb_schedule_export(ldpcb_schedule s, int32_t* grp_off, int32_t* grp_cns) {
+  return guard([&] {
+    need(s != nullptr, "null handle");
+    const auto& h = s->impl->host;
+    if (grp_off) std::memcpy(grp_off, h.grp_off.data(), h.grp_off.size() * sizeof(int32_t));
+    if (grp_cns) std::memcpy(grp_cns, h.grp_cns.data(), h.grp_cns.size() * sizeof(int32_t));
+    return LDPCB_OK;
+  });
+}
+
+int ldpcb_schedule_iteration_budget(ldpcb_schedule s, int i_max, int32_t* budget) {
+  return guard([&] {
+    need(s != nullptr && budget != nullptr, "null argument");
+    *budget = ldpcb::iteration_budget(s->impl->host, s->impl->code->host.m, i_max);
+    return LDPCB_OK;
+  });
+}
+
+int ldpcb_schedule_cocsg(ldpcb_schedule s, int32_t* counts) {
+  return guard([&] {
+    need(s != nullptr && counts != nullptr, "null argument");
+    const auto v = ldpcb::measure_cocsg(s->impl->code->host, s->impl->host);
+    std::copy(v.begin(), v.end(), counts);
+    return LDPCB_OK;
+  });
+}
+
+void ldpcb_schedule_destroy(ldpcb_schedule s) { delete s; }
+
+int ldpcb_sigma2_from_ebn0(double ebn0_db, double rate, double* sigma2) {
+  return guard([&] {
+    need(rate > 0.0 && rate <= 1.0, "code rate must be in (0, 1]");
+    need(sigma2 != nullptr, "null output");
+    *sigma2 = ldpcb::awgn_sigma2(ebn0_db, rate);
+    return LDPCB_OK;
+  });
+}
+
+int ldpcb_channel_llr_device(int n, double sigma2, uint64_t seed, int64_t frame0, int64_t frames, float* d_llr,
+                             void* stream) {
+  return guard([&] {
+    need(n >= 1, "frame length must be >= 1");
+    need(frames >= 0 && (frames == 0 || d_llr != nullptr), "bad frame buffer");
+    need(sigma2 > 0.0, "sigma2 must be positive");
+    launch(ldpcb::launch_channel(n, sigma2, seed, frame0, frames, d_llr, stream), "channel kernel");
+    return LDPCB_OK;
+  });
+}
+
+int ldpcb_decode_device(ldpcb_code code, ldpcb_schedule s, int64_t frames, const float* d_llr, int max_iters,
+                        int early_stop, uint8_t* d_bits, int bits_packed, int32_t* d_iterations, uint8_t* d_converged,
+                        float* d_posterior, int32_t* d_trace, int64_t* d_counters, void* stream) {
+  return guard([&] {
+    need(max_iters >= 1, "max_iters must be >= 1");
+    need(frames >= 0, "frames must be >= 0");
+    need(frames == 0 || d_llr != nullptr, "null LLR buffer");
+    const auto g = dev_graph(code, s);
+    ldpcb::DecodeArgs a;
+    a.frames = frames;
+    a.llr = d_llr;
+    a.max_iters = max_iters;
+    a.early_stop = early_stop != 0;
+    a.bits = d_bits;
+    a.bits_packed = bits_packed != 0;
+    a.iterations = d_iterations;
+    a.converged = d_converged;
+    a.posterior = d_posterior;
+    a.trace = d_trace;
+    a.counters = reinterpret_cast<unsigned long long*>(d_counters);
+    ldpcb::Plan p;
+    const int err = ldpcb::launch_decode(g, a, stream, &p);
+    if (p.kernel == 0) throw std::runtime_error("no resident decoder plan fits this code (n too large)");
+    launch(err, "decode kernel");
+    return LDPCB_OK;
+  });
+}
+
+int ldpcb_decode_host(ldpcb_code code, ldpcb_schedule s, int64_t frames, const float* llr, int max_iters,
+                      int early_stop, uint8_t* bits, int bits_packed, int32_t* iterations, uint8_t* converged,
+                      float* posterior, int64_t* counters) {
+  return guard([&] {
+    need(max_iters >= 1, "max_iters must be >= 1");
+    need(frames >= 0, "frames must be >= 0");
+    need(frames == 0 || llr != nullptr, "null LLR buffer");
+    if (frames == 0) return LDPCB_OK;
+    const auto g = dev_graph(code, s);
+    const int n = g.n;
+    const int64_t nb = bits_packed ? (n + 7) / 8 : n;
+    const ldpcb::Plan p0 = ldpcb::plan_decode(g, frames);
+    if (p0.kernel == 0) throw std::runtime_error("no resident decoder plan fits this code (n too large)");
+    // chunks of ~32 MB of LLRs, a multiple of the frames per CTA
+    int64_t chunk = std::max<int64_t>(p0.fpc, (int64_t{32} << 20) / (4 * n));
+    chunk = std::min<int64_t>(chunk, frames);
+    chunk = (chunk + p0.fpc - 1) / p0.fpc * p0.fpc;
+    const int kSlots = 2;
+    cudaStream_t st[kSlots];
+    struct Buf {
+      float* llr = nullptr;
+      uint8_t* bits = nullptr;
+      int32_t* it = nullptr;
+      uint8_t* cv = nullptr;
+      float* post = nullptr;
+      int64_t* cnt = nullptr;
+    } buf[kSlots];
+    for (int k = 0; k < kSlots; ++k) {
+      cuda_check(cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking), "cudaStreamCreate");
+      cuda_check(cudaMallocAsync(&buf[k].llr, chunk * n * sizeof(float), st[k]), "cudaMallocAsync");
+      if (bits) cuda_check(cudaMallocAsync(&buf[k].bits, chunk * nb, st[k]), "cudaMallocAsync");
+      if (iterations) cuda_check(cudaMallocAsync(&buf[k].it, chunk * sizeof(int32_t), st[k]), "cudaMallocAsync");
+      if (converged) cuda_check(cudaMallocAsync(&buf[k].cv, chunk, st[k]), "cudaMallocAsync");
+      if (posterior) cuda_check(cudaMallocAsync(&buf[k].post, chunk * n * sizeof(float), st[k]), "cudaMallocAsync");
+      if (counters) {
+        cuda_check(cudaMallocAsync(&buf[k].cnt, 6 * sizeof(int64_t), st[k]), "cudaMallocAsync");
+        cuda_check(cudaMemsetAsync(buf[k].cnt, 0, 6 * sizeof(int64_t), st[k]), "cudaMemsetAsync");
+      }
+    }
+    int64_t slot = 0;
+    for (int64_t c0 = 0; c0 < frames; c0 += chunk, ++slot) {
+      const int k = static_cast<int>(slot % kSlots);
+      const int64_t cnt = std::min(chunk, frames - c0);
+      cuda_check(cudaMemcpyAsync(buf[k].llr, llr + c0 * n, cnt * n * sizeof(float), cudaMemcpyHostToDevice, st[k]),
+                 "H2D");
+      ldpcb::DecodeArgs a;
+      a.frames = cnt;
+      a.llr = buf[k].llr;
+      a.max_iters = max_iters;
+      a.early_stop = early_stop != 0;
+      a.bits = buf[k].bits;
+      a.bits_packed = bits_packed != 0;
+      a.iterations = buf[k].it;
+      a.converged = buf[k].cv;
+      a.posterior = buf[k].post;
+      a.counters = reinterpret_cast<unsigned long long*>(buf[k].cnt);
+      launch(ldpcb::launch_decode(g, a, st[k], nullptr), "decode kernel");
+      if (bits) cuda_check(cudaMemcpyAsync(bits + c0 * nb, buf[k].bits, cnt * nb, cudaMemcpyDeviceToHost, st[k]), "D2H");
+      if (iterations)
+        cuda_check(cudaMemcpyAsync(iterations + c0, buf[k].it, cnt * sizeof(int32_t), cudaMemcpyDeviceToHost, st[k]),
+                   "D2H");
+      if (converged) cuda_check(cudaMemcpyAsync(converged + c0, buf[k].cv, cnt, cudaMemcpyDeviceToHost, st[k]), "D2H");
+      if (posterior)
+        cuda_check(cudaMemcpyAsync(posterior + c0 * n, buf[k].post, cnt * n * sizeof(float), cudaMemcpyDeviceToHost,
+                                   st[k]),
+                   "D2H");
+    }
+    int64_t total[6] = {0, 0, 0, 0, 0, 0};
+    for (int k = 0; k < kSlots; ++k) {
+      if (counters) {
+        int64_t h[6];
+        cuda_check(cudaMemcpyAsync(h, buf[k].cnt, sizeof h, cudaMemcpyDeviceToHost, st[k]), "D2H");
+        cuda_check(cudaStreamSynchronize(st[k]), "sync");
+        for (int i = 0; i < 6; ++i) total[i] += h[i];
+      }
+      cudaFreeAsync(buf[k].llr, st[k]);
+      if (buf[k].bits) cudaFreeAsync(buf[k].bits, st[k]);
+      if (buf[k].it) cudaFreeAsync(buf[k].it, st[k]);
+      if (buf[k].cv) cudaFreeAsync(buf[k].cv, st[k]);
+      if (buf[k].post) cudaFreeAsync(buf[k].post, st[k]);
+      if (buf[k].cnt) cudaFreeAsync(buf[k].cnt, st[k]);
+      cuda_check(cudaStreamSynchronize(st[k]), "sync");
+      cudaStreamDestroy(st[k]);
+    }
+    if (counters)
+      for (int i = 0; i < 6; ++i) counters[i] += total[i];
+    return LDPCB_OK;
+  });
+}
+
+int ldpcb_simulate_device(ldpcb_code code, ldpcb_schedule s, double sigma2, uint64_t channel_seed, int64_t frame_begin,
+                          int64_t frames, int max_iters, int early_stop, int64_t* d_counters, void* stream) {
+  return guard([&] {
+    need(max_iters >= 1, "max_iters must be >= 1");
+    need(frames >= 0 && frame_begin >= 0, "bad frame range");
+    need(sigma2 > 0.0, "sigma2 must be positive");
+    need(d_counters != nullptr, "null counters");
+    if (frames == 0) return LDPCB_OK;
+    const auto g = dev_graph(code, s);
+    const ldpcb::Plan p0 = ldpcb::plan_decode(g, frames);
+    if (p0.kernel == 0) throw std::runtime_error("no resident decoder plan fits this code (n too large)");
+    auto st = static_cast<cudaStream_t>(stream);
+    int64_t chunk = std::max<int64_t>(p0.fpc, (int64_t{256} << 20) / (4 * g.n));
+    chunk = std::min<int64_t>(chunk, frames);
+    float* scratch = nullptr;
+    cuda_check(cudaMallocAsync(&scratch, chunk * g.n * sizeof(float), st), "cudaMallocAsync");
+    for (int64_t c0 = 0; c0 < frames; c0 += chunk) {
+      const int64_t cnt = std::min(chunk, frames - c0);
+      launch(ldpcb::launch_channel(g.n, sigma2, channel_seed, frame_begin + c0, cnt, scratch, stream), "channel");
+      ldpcb::DecodeArgs a;
+      a.frames = cnt;
+      a.llr = scratch;
+      a.max_iters = max_iters;
+      a.early_stop = early_stop != 0;
+      a.counters = reinterpret_cast<unsigned long long*>(d_counters);
+      launch(ldpcb::launch_decode(g, a, stream, nullptr), "decode kernel");
+    }
+    cuda_check(cudaFreeAsync(scratch, st), "cudaFreeAsync");
+    return LDPCB_OK;
+  });
+}
+
+int ldpcb_check_update_device(int degree, int64_t rows, const float* d_v2c, float* d_c2v, void* stream) {
+  return guard([&] {
+    need(degree >= 2 && degree <= 32, "degree must be in [2, 32]");
+    need(rows >= 0, "rows must be >= 0");
+    launch(ldpcb::launch_check_update(degree, rows, d_v2c, d_c2v, stream), "check_update kernel");
+    return LDPCB_OK;
+  });
+}
+
+int ldpcb_run_subiterations_device(ldpcb_code code, ldpcb_schedule s, int64_t frames, const float* d_llr,
+                                   int n_subiters, float* d_c2v, float* d_v2c, void* stream) {
+  return guard([&] {
+    need(n_subiters >= 1, "n_subiters must be >= 1");
+    const auto g = dev_graph(code, s);
+    ldpcb::DecodeArgs a;
+    a.frames = frames;
+    a.llr = d_llr;
+    a.max_iters = n_subiters / g.G + 1;
+    a.early_stop = 0;
+    a.max_subiters = n_subiters;
+    a.c2v_out = d_c2v;
+    a.v2c_out = d_v2c;
+    ldpcb::Plan p;
+    const int err = ldpcb::launch_decode(g, a, stream, &p);
+    if (p.kernel == 0) throw std::runtime_error("no resident decoder plan fits this code (n too large)");
+    launch(err, "decode kernel");
+    return LDPCB_OK;
+  });
+}
+
+int ldpcb_decode_plan(ldpcb_code code, ldpcb_schedule s, int64_t frames, int32_t* kernel, int32_t* fpc,
+                      int32_t* threads, int32_t* smem_bytes, int32_t* degree_bucket) {
+  return guard([&] {
+    const auto g = dev_graph(code, s);
+    const auto p = ldpcb::plan_decode(g, frames);
+    if (kernel) *kernel = p.kernel;
+    if (fpc) *fpc = p.fpc;
+    if (threads) *threads = p.threads;
+    if (smem_bytes) *smem_bytes = p.smem;
+    if (degree_bucket) *degree_bucket = p.degree_bucket;
+    return LDPCB_OK;
+  });
+}
+
+int ldpcb_set_tuning(int frames_per_cta, int threads) {
+  return guard([&] {
+    need(frames_per_cta == 0 || frames_per_cta == 1 || frames_per_cta == 2 || frames_per_cta == 4 ||
+             frames_per_cta == 8 || frames_per_cta == 16,
+         "frames_per_cta must be 0 (auto) or a power of two <= 16");
+    need(threads == 0 || (threads >= 32 && threads <= 512 && threads % 32 == 0),
+         "threads must be 0 (auto) or a multiple of 32 in [32, 512]");
+    ldpcb::set_tuning(frames_per_cta, threads);
+    return LDPCB_OK;
+  });
+}
+
+int64_t ldpcb_kernel_launches(void) { return ldpcb::kernel_launch_count(); }
+
+}  // extern "C"

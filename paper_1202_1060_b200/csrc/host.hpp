@@ -1,0 +1,95 @@
+// host.hpp -- host-side code graphs and CN-group schedules.
+//
+// This is the single source of truth for H and the grouping: the B200 kernels
+// and the CPU oracle both consume the arrays built here, so construction and
+// grouping are bit-exact by construction.
+//
+// Reference interfaces mirrored:
+//   CodeData      <- ldpc::TannerGraph            tanner.hpp:21-37
+//   build_code    <- ldpc::build_from_check_lists tanner.hpp:79-114
+//   regular_rows  <- ldpc::random_regular_graph   tanner.hpp:356-393
+//   parse_alist / serialize_alist                 tanner.hpp:163-317
+//   ScheduleData  <- ldpc::GroupSchedule          schedule.hpp:32-40
+//   random_groups <- detail::generate_groups      schedule.hpp:54-115
+//   iteration_budget / measure_cocsg              schedule.hpp:175-210
+#pragma once
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <vector>
+
+namespace ldpcb {
+
+using Rows = std::vector<std::vector<int>>;
+
+// CN-major edge numbering: edge (check m, slot k) = row_off[m] + k. The VN
+// view lists CN ids ascending with the matching edge ids.
+struct CodeData {
+  int n = 0, m = 0, E = 0;
+  int max_cdeg = 0, max_vdeg = 0;
+  std::vector<int32_t> row_off, cols;
+  std::vector<int32_t> var_off, var_cns, var_edges;
+};
+
+// Alist errors carry the reference's kind enumeration and 1-based line.
+enum class AlistKind {
+  malformed_header = 0,
+  bad_token,
+  degree_error,
+  length_mismatch,
+  index_out_of_range,
+  duplicate_entry,
+  edge_count_mismatch,
+  transpose_mismatch,
+  trailing_content,
+  truncated,
+};
+
+struct AlistFailure : std::runtime_error {
+  AlistKind kind;
+  int line;
+  AlistFailure(AlistKind k, int l, const std::string& what)
+      : std::runtime_error("alist parse error at line " + std::to_string(l) + ": " + what), kind(k), line(l) {}
+};
+
+CodeData build_code(int n_vars, const Rows& rows);
+Rows rows_of(const CodeData& c);
+
+Rows regular_rows(int n_vars, int dv, int dc, uint64_t seed);
+// Edge swaps until no two CNs share two VNs (girth >= 6); degrees preserved.
+void break_4cycles(int n_vars, Rows& rows, uint64_t seed);
+// Quasi-cyclic base-matrix expansion (BASELINE config 3).
+Rows qc_rows(int base_rows, int base_cols, int z, double p_empty, int min_col_degree, uint64_t seed);
+// Socket-matched irregular VN / regular CN ensemble (BASELINE config 4).
+Rows irregular_rows(int n_vars, const std::vector<int>& degrees, const std::vector<int>& counts, int dc,
+                    uint64_t seed);
+int64_t count_4cycles(const CodeData& c);
+
+CodeData parse_alist(std::string_view text);
+std::string serialize_alist(const CodeData& c);
+
+enum class Kind { flooding = 0, disjoint = 1, nondisjoint = 2 };
+
+struct ScheduleData {
+  Kind kind = Kind::flooding;
+  int G = 1;
+  double overlap = 0.0;
+  int group_size = 0;
+  uint64_t seed = 0;
+  std::vector<int32_t> grp_off, grp_cns;      // groups in processing order
+  std::vector<int32_t> touch_off, touch_vns;  // sorted unique VNs per group
+  int64_t edge_updates_per_iter = 0;          // sum of CN degrees over group slots
+  int64_t touched_per_iter = 0;               // sum of touched-set sizes
+  int max_group = 0, max_touched = 0;
+};
+
+ScheduleData schedule_from_groups(const CodeData& c, Kind kind, const Rows& groups);
+ScheduleData flooding_schedule(const CodeData& c);
+ScheduleData reference_random_schedule(const CodeData& c, Kind kind, int G, double overlap, uint64_t seed);
+ScheduleData window_schedule(const CodeData& c, Kind kind, int G, int window, int stride);
+Rows random_groups(int M, int G, double overlap, uint64_t stream_seed_value);
+int iteration_budget(const ScheduleData& s, int n_checks, int i_max);
+std::vector<int> measure_cocsg(const CodeData& c, const ScheduleData& s);
+
+}  // namespace ldpcb
