@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""Throughput benchmark: BASELINE.json's metric (decoded info bits/s at fixed
+iterations) on its throughput configuration (config 5).
+
+Default workload "c5_n1008": the (3,6)-regular n=1008 code with 4-cycles
+removed, NDGSBP (8 windows of 84 CNs at stride 63), Eb/N0 = 2.0 dB, exactly 10
+iterations (no early stop). One step = one decode of a batch of frames per GPU
+whose fp32 LLRs are already resident in HBM (generated on the device with the
+reference's channel stream, frame ids sharded by rank), followed by the NCCL
+allreduce of the int64[6] error / iteration counters.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference]
+
+Under torchrun each rank decodes its own frame range (weak scaling); rank 0
+prints one JSON line. `--impl reference` runs the reference CPU decoder
+(oracle/_ref: the unmodified reference headers, else the C port) on all host
+cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decoded info bits/s at fixed iterations"
+UNIT = "info bits/s"
+MUFU_PER_EDGE = 3  # SASS-counted: 1 MUFU.EX2 + 2 MUFU.LG2 per CN-edge update (decoder.cu)
+MUFU_PER_SM_CLK = 16
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", default="c5_n1008")
+    ap.add_argument("--frames", type=int, default=1 << 21, help="frames per step per GPU")
+    ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU sample duration")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload(name):
+    import paper_1202_1060_b200 as P
+
+    if name == "c5_n1008":
+        g = P.configs.c1_code()
+        s = P.configs.c1_schedules(g)["ndgsbp"]
+        desc = "C5: (3,6)-regular n=1008 girth>=6 (seed 1), NDGSBP 8 windows x 84 CNs stride 63, Eb/N0 2.0 dB"
+        return g, s, 2.0, desc
+    raise SystemExit(f"unknown workload {name}")
+
+
+def mean_sigma2(P, g, ebn0):
+    return P.sigma2_from_ebn0(ebn0, g.rate)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def reference_cpu(g, s, sigma2, iters, target_s, frames_hint=None):
+    """Time the reference CPU decoder on all host threads on a bounded sample.
+    Returns (info_bits_per_s, frames, seconds, threads, kind)."""
+    from oracle.oracle import best_available
+
+    orc = best_available()
+    threads = os.cpu_count() or 1
+    og = orc.graph(g.n_vars, *g.csr())
+    groups = s.groups
+    K = g.n_vars - g.n_checks
+    cal = max(threads * 4, 64)
+    llr = orc.transmit_batch_f32(sigma2, 1, g.n_vars, 0, cal, threads)
+    t0 = time.perf_counter()
+    orc.decode_batch(og, groups, llr, iters, early_stop=False, threads=threads)
+    dt = time.perf_counter() - t0
+    frames = frames_hint or max(cal, int(cal * target_s / max(dt, 1e-6)))
+    llr = orc.transmit_batch_f32(sigma2, 1, g.n_vars, 0, frames, threads)
+    t0 = time.perf_counter()
+    orc.decode_batch(og, groups, llr, iters, early_stop=False, threads=threads)
+    dt = time.perf_counter() - t0
+    return frames * K / dt, frames, dt, threads, orc.kind
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import paper_1202_1060_b200 as P
+
+    g, s, ebn0, desc = workload(args.workload)
+    sigma2 = mean_sigma2(P, g, ebn0)
+    per_step = max(1.0, args.cpu_seconds / max(args.steps, 1))
+    vals = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        v, frames, dt, threads, kind = reference_cpu(g, s, sigma2, args.iters, per_step,
+                                                     frames_hint=info[1] if info else None)
+        info = (v, frames, dt, threads, kind)
+        if i >= args.warmup:
+            vals.append((v, dt))
+    value = statistics.median(v for v, _ in vals)
+    ms = statistics.median(dt for _, dt in vals) * 1e3
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (reference channel stream, seed 1)",
+        "config": {"workload": desc + f", {args.iters} fixed iterations", "frames_per_step": info[1],
+                   "host_threads": info[3]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": info[3], "kind": info[4],
+                         "sample": f"{info[1]} frames per step of the same workload"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1202_1060_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    g, s, ebn0, desc = workload(args.workload)
+    sigma2 = mean_sigma2(P, g, ebn0)
+    B = args.frames
+    n = g.n_vars
+    K = n - g.n_checks
+    stream = torch.cuda.current_stream()
+
+    # inputs resident in HBM: this rank's frame ids [rank*B, (rank+1)*B)
+    llr = P.transmit_all_zero(n, sigma2, 1, rank * B, B)
+    bits = torch.empty((B, (n + 7) // 8), dtype=torch.uint8, device=dev)
+    its = torch.empty(B, dtype=torch.int32, device=dev)
+    conv = torch.empty(B, dtype=torch.uint8, device=dev)
+    counters = torch.zeros(6, dtype=torch.int64, device=dev)
+    pl = P.plan(g, s, B)
+
+    def step(ev=None):
+        counters.zero_()
+        if ev:
+            ev[0].record(stream)
+        P.api.check(P.api.lib.ldpcb_decode_device(
+            g.handle, s.handle, B, P.api._vp(llr), args.iters, 0, P.api._vp(bits), 1, P.api._vp(its),
+            P.api._vp(conv), None, None, P.api._vp(counters), P.api._stream()))
+        if ev:
+            ev[1].record(stream)
+        if world > 1:
+            dist.all_reduce(counters)  # NCCL: int64[6] counters across ranks
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = P.kernel_launches()
+    with ClockSampler(local) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for i in range(args.steps):
+            step(evs[i])
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+    launches = P.kernel_launches() - launches0
+    elapsed_ms = t0.elapsed_time(t1)
+    kernel_ms = statistics.mean(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t.item())
+    total_frames = B * args.steps * world
+    value = total_frames * K / (elapsed_ms / 1e3)
+    cnt = counters.cpu().tolist()
+
+    # ---- roofline of the dominant kernel (SFU / MUFU issue rate)
+    edge_updates = s.edge_updates_per_iter * args.iters * B
+    mufu_achieved = edge_updates * MUFU_PER_EDGE / (kernel_ms / 1e3)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        pass
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    mufu_peak = n_sm * MUFU_PER_SM_CLK * sm_max * 1e6
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "r01_dram_bytes_per_launch.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(args.workload)
+        except (OSError, ValueError):
+            traffic = None
+
+    # ---- end to end through the host C-ABI call (pinned host buffers)
+    e2e = None
+    if not args.no_e2e:
+        Be = B
+        h_llr = torch.empty((Be, n), dtype=torch.float32, pin_memory=True)
+        h_llr.copy_(llr[:Be].cpu())
+        h_bits = torch.empty((Be, (n + 7) // 8), dtype=torch.uint8, pin_memory=True)
+        h_cnt = torch.zeros(6, dtype=torch.int64)
+        for _ in range(2):
+            P.decode_host(g, s, h_llr, args.iters, early_stop=False, packed=True, bits=h_bits, counters=h_cnt)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e_steps = max(1, min(args.steps, 5))
+        t_start = time.perf_counter()
+        for _ in range(e_steps):
+            h_cnt.zero_()
+            P.decode_host(g, s, h_llr, args.iters, early_stop=False, packed=True, bits=h_bits, counters=h_cnt)
+        e_dt = time.perf_counter() - t_start
+        te = torch.tensor([e_dt], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e_dt = float(te.item())
+        e2e = {"value": Be * e_steps * world * K / e_dt, "unit": UNIT, "h2d_bytes_per_step": Be * n * 4,
+               "d2h_bytes_per_step": Be * ((n + 7) // 8) + 48,
+               "api": "ldpcb_decode_host (pinned host LLRs in, packed bits + counters out)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, frames, dt, threads, kind = reference_cpu(g, s, sigma2, args.iters, args.cpu_seconds)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
+               "sample": f"{frames} frames of the same workload ({dt:.1f} s, {threads} threads)"}
+
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": elapsed_ms / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic (device port of the reference channel stream, seed 1)",
+            "config": {
+                "workload": desc + f", {args.iters} fixed iterations, no early stop",
+                "frames_per_step_per_gpu": B,
+                "parallelism": f"frames sharded over {world} GPU(s), NCCL allreduce of int64[6] counters",
+                "l2": f"inputs ({B * n * 4 / 1e9:.1f} GB per GPU) larger than L2; no flush",
+                "plan": pl,
+            },
+            "frames_per_s": total_frames / (elapsed_ms / 1e3),
+            "edge_updates_per_s": edge_updates * args.steps * world / (elapsed_ms / 1e3),
+            "roofline": {
+                "bound": "sfu",
+                "achieved": mufu_achieved / 1e9,
+                "peak": mufu_peak / 1e9,
+                "unit": "GMUFU/s",
+                "frac": mufu_achieved / mufu_peak,
+                "traffic": traffic,
+                "note": f"decode kernel: {MUFU_PER_EDGE} MUFU per CN-edge update x {s.edge_updates_per_iter} "
+                        f"edge updates/iter x {args.iters} iters x {B} frames per launch / CUDA-event launch time "
+                        f"{kernel_ms:.3f} ms; peak = {n_sm} SMs x {MUFU_PER_SM_CLK}/clk x {sm_max:.0f} MHz "
+                        "(MEASURED_PEAKS sm_max_mhz)",
+            },
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "counters": dict(zip(P.COUNTER_NAMES, cnt)),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

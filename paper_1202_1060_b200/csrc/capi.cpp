@@ -57,11 +57,6 @@ T* upload(const std::vector<T>& v) {
   return d;
 }
 
-struct DevArrays {
-  std::vector<void*> ptrs;
-  ~DevArrays() {}
-};
-
 void free_on(int dev, std::vector<void*>& ptrs) {
   int cur = -1;
   if (cudaGetDevice(&cur) != cudaSuccess) return;
@@ -76,7 +71,7 @@ struct CodeImpl {
   bool cregular = true, vregular = true;
   std::mutex mu;
   struct Dev {
-    int32_t *row_off, *cols, *var_off, *var_edges;
+    int32_t* cols;
     std::vector<void*> ptrs;
   };
   std::map<int, Dev> dev;
@@ -95,11 +90,8 @@ struct CodeImpl {
     auto it = dev.find(d);
     if (it != dev.end()) return it->second;
     Dev x;
-    x.row_off = upload(host.row_off);
     x.cols = upload(host.cols);
-    x.var_off = upload(host.var_off);
-    x.var_edges = upload(host.var_edges);
-    x.ptrs = {x.row_off, x.cols, x.var_off, x.var_edges};
+    x.ptrs = {x.cols};
     return dev.emplace(d, std::move(x)).first->second;
   }
 };
@@ -107,9 +99,10 @@ struct CodeImpl {
 struct SchedImpl {
   std::shared_ptr<CodeImpl> code;
   ldpcb::ScheduleData host;
+  ldpcb::KernelTables tables;
   std::mutex mu;
   struct Dev {
-    int32_t *grp_off, *grp_cns, *touch_off, *touch_vns;
+    int32_t *cn_off, *cn_rec, *vn_off, *vn_rec, *all_rec;
     std::vector<void*> ptrs;
   };
   std::map<int, Dev> dev;
@@ -124,11 +117,12 @@ struct SchedImpl {
     auto it = dev.find(d);
     if (it != dev.end()) return it->second;
     Dev x;
-    x.grp_off = upload(host.grp_off);
-    x.grp_cns = upload(host.grp_cns);
-    x.touch_off = upload(host.touch_off);
-    x.touch_vns = upload(host.touch_vns);
-    x.ptrs = {x.grp_off, x.grp_cns, x.touch_off, x.touch_vns};
+    x.cn_off = upload(tables.cn_off);
+    x.cn_rec = upload(tables.cn_rec);
+    x.vn_off = upload(tables.vn_off);
+    x.vn_rec = upload(tables.vn_rec);
+    x.all_rec = upload(tables.all_rec);
+    x.ptrs = {x.cn_off, x.cn_rec, x.vn_off, x.vn_rec, x.all_rec};
     return dev.emplace(d, std::move(x)).first->second;
   }
 };
@@ -159,6 +153,8 @@ int make_sched(const std::shared_ptr<CodeImpl>& code, ldpcb::ScheduleData s, ldp
   auto impl = std::make_shared<SchedImpl>();
   impl->code = code;
   impl->host = std::move(s);
+  const int bucket = ldpcb::cn_bucket(code->host.max_cdeg, code->cregular);
+  if (bucket > 0) impl->tables = ldpcb::kernel_tables(code->host, impl->host, ldpcb::cn_record_stride(bucket));
   *out = new ldpcb_schedule_s{impl};
   return LDPCB_OK;
 }
@@ -178,14 +174,18 @@ ldpcb::DevGraph dev_graph(ldpcb_code code, ldpcb_schedule s) {
   g.max_vdeg = h.max_vdeg;
   g.cregular = code->impl->cregular;
   g.vregular = code->impl->vregular;
-  g.row_off = c.row_off;
+  const auto& t = s->impl->tables;
+  if (t.cs == 0) throw std::runtime_error("check-node degree above 32 is not supported by the resident kernel");
+  g.cs = t.cs;
+  g.vs4 = t.vs4;
+  g.max_cn_items = t.max_cn_items;
+  g.max_vn_items = t.max_vn_items;
   g.cols = c.cols;
-  g.var_off = c.var_off;
-  g.var_edges = c.var_edges;
-  g.grp_off = d.grp_off;
-  g.grp_cns = d.grp_cns;
-  g.touch_off = d.touch_off;
-  g.touch_vns = d.touch_vns;
+  g.cn_off = d.cn_off;
+  g.cn_rec = d.cn_rec;
+  g.vn_off = d.vn_off;
+  g.vn_rec = d.vn_rec;
+  g.all_rec = d.all_rec;
   return g;
 }
 
@@ -622,8 +622,8 @@ int ldpcb_set_tuning(int frames_per_cta, int threads) {
     need(frames_per_cta == 0 || frames_per_cta == 1 || frames_per_cta == 2 || frames_per_cta == 4 ||
              frames_per_cta == 8 || frames_per_cta == 16,
          "frames_per_cta must be 0 (auto) or a power of two <= 16");
-    need(threads == 0 || (threads >= 32 && threads <= 512 && threads % 32 == 0),
-         "threads must be 0 (auto) or a multiple of 32 in [32, 512]");
+    need(threads == 0 || (threads >= 32 && threads <= 1024 && threads % 32 == 0),
+         "threads must be 0 (auto) or a multiple of 32 in [32, 1024]");
     ldpcb::set_tuning(frames_per_cta, threads);
     return LDPCB_OK;
   });

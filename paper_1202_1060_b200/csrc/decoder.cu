@@ -106,7 +106,7 @@ __device__ __forceinline__ void boxplus_row(const float (&x)[D], int deg, Store&
 }
 
 struct Shared {
-  float* c2v;  // [E][FPC]
+  float* c2v;  // [(E+1)][FPC]; slot E stays zero (pads short VN records)
   float* P;    // [n][FPC] posterior (channel + all c2v), unclamped
   float* L;    // [n][FPC] clamped channel LLR
   int* done;   // [FPC]
@@ -116,47 +116,84 @@ struct Shared {
   int* berr;
 };
 
+// One CN record (host.hpp KernelTables) -> the clamped incoming messages
+// v2c = clamp(P_v - c2v_e) (posterior form of var_update, decoder.hpp:91-105).
+template <int D, bool EXACT>
+struct CnRecord {
+  static constexpr int kInts = (2 + D + 3) / 4 * 4;
+  int r[kInts];
+  __device__ __forceinline__ explicit CnRecord(const int32_t* __restrict__ p) {
+    const int4* q = reinterpret_cast<const int4*>(p);
+#pragma unroll
+    for (int i = 0; i < kInts / 4; ++i) {
+      const int4 t = __ldg(q + i);
+      r[4 * i] = t.x;
+      r[4 * i + 1] = t.y;
+      r[4 * i + 2] = t.z;
+      r[4 * i + 3] = t.w;
+    }
+  }
+  __device__ __forceinline__ int off() const { return r[0]; }
+  __device__ __forceinline__ int deg() const { return EXACT ? D : r[1]; }
+  __device__ __forceinline__ int var(int k) const { return r[2 + k]; }
+};
+
 template <int D, bool EXACT, int FPC>
-__device__ __forceinline__ void cn_update(const DevGraph& g, const Shared& s, int r, unsigned f) {
-  const int off = __ldg(g.row_off + r);
-  const int deg = EXACT ? D : __ldg(g.row_off + r + 1) - off;
+__device__ __forceinline__ void cn_update(const Shared& s, const int32_t* __restrict__ rec, unsigned f) {
+  const CnRecord<D, EXACT> cr(rec);
+  const int off = cr.off(), deg = cr.deg();
   float x[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     x[k] = 0.f;
-    if (EXACT || k < deg) {
-      const int v = __ldg(g.cols + off + k);
-      x[k] = clamp_llr(s.P[v * FPC + f] - s.c2v[(off + k) * FPC + f]);
-    }
+    if (EXACT || k < deg) x[k] = clamp_llr(s.P[cr.var(k) * FPC + f] - s.c2v[(off + k) * FPC + f]);
   }
   boxplus_row<D, EXACT>(x, deg, [&](int k, float c) { s.c2v[(off + k) * FPC + f] = c; });
 }
 
-template <int FPC>
-__device__ __forceinline__ void vn_refresh(const DevGraph& g, const Shared& s, int v, unsigned f) {
-  const int a = __ldg(g.var_off + v), b = __ldg(g.var_off + v + 1);
+// P_v = L_v + sum of c2v over the VN's edges in ascending-CN order (the
+// totals of decoder.hpp:162-165; refreshes every v2c of v at once).
+template <int FPC, int VS>
+__device__ __forceinline__ void vn_refresh(const Shared& s, const int4* __restrict__ rec, int vs4, unsigned f) {
+  int4 t = __ldg(rec);
+  const int v = t.x;
   float acc = s.L[v * FPC + f];
-  for (int j = a; j < b; ++j) acc += s.c2v[__ldg(g.var_edges + j) * FPC + f];
+  acc += s.c2v[t.y * FPC + f];
+  acc += s.c2v[t.z * FPC + f];
+  acc += s.c2v[t.w * FPC + f];
+  const int nq = VS > 0 ? VS : vs4;
+#pragma unroll
+  for (int q = 1; q < nq; ++q) {
+    t = __ldg(rec + q);
+    acc += s.c2v[t.x * FPC + f];
+    acc += s.c2v[t.y * FPC + f];
+    acc += s.c2v[t.z * FPC + f];
+    acc += s.c2v[t.w * FPC + f];
+  }
   s.P[v * FPC + f] = acc;
 }
 
-template <int FPC>
-__device__ __forceinline__ unsigned parity(const DevGraph& g, const Shared& s, int r, unsigned f) {
-  const int a = __ldg(g.row_off + r), b = __ldg(g.row_off + r + 1);
+template <int D, bool EXACT, int FPC>
+__device__ __forceinline__ unsigned parity(const Shared& s, const int32_t* __restrict__ rec, unsigned f) {
+  const CnRecord<D, EXACT> cr(rec);
   unsigned p = 0;
-  for (int e = a; e < b; ++e) p ^= static_cast<unsigned>(s.P[__ldg(g.cols + e) * FPC + f] < 0.f);
+#pragma unroll
+  for (int k = 0; k < D; ++k)
+    if (EXACT || k < cr.deg()) p ^= static_cast<unsigned>(s.P[cr.var(k) * FPC + f] < 0.f);
   return p;
 }
 
-template <int D, bool EXACT, int FPC>
-__global__ void __launch_bounds__(512) decode_resident(const DevGraph g, const DecodeArgs a) {
+constexpr int max_threads_for(int D) { return D <= 8 ? 1024 : 512; }
+
+template <int D, bool EXACT, int FPC, int VS>
+__global__ void __launch_bounds__(max_threads_for(D)) decode_resident(const DevGraph g, const DecodeArgs a) {
   extern __shared__ __align__(16) float smem[];
   __shared__ int s_active;
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int n = g.n, E = g.E;
+  const int n = g.n, E = g.E, cs = g.cs;
   Shared s;
   s.c2v = smem;
-  s.P = s.c2v + static_cast<size_t>(E) * FPC;
+  s.P = s.c2v + static_cast<size_t>(E + 1) * FPC;
   s.L = s.P + static_cast<size_t>(n) * FPC;
   s.done = reinterpret_cast<int*>(s.L + static_cast<size_t>(n) * FPC);
   s.weight = s.done + FPC;
@@ -176,10 +213,10 @@ __global__ void __launch_bounds__(512) decode_resident(const DevGraph g, const D
     s.P[v * FPC + f] = x;
   }
   {
+    const int total = (E + 1) * FPC;
     float4* c4 = reinterpret_cast<float4*>(s.c2v);
-    const int n4 = (E * FPC) / 4;
-    for (int i = tid; i < n4; i += nt) c4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int i = n4 * 4 + tid; i < E * FPC; i += nt) s.c2v[i] = 0.f;
+    for (int i = tid; i < total / 4; i += nt) c4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = total / 4 * 4 + tid; i < total; i += nt) s.c2v[i] = 0.f;
   }
   if (tid < FPC) {
     s.done[tid] = tid >= nf;
@@ -198,20 +235,23 @@ __global__ void __launch_bounds__(512) decode_resident(const DevGraph g, const D
     for (int grp = 0; grp < g.G; ++grp) {
       if (dump && sub == a.max_subiters) goto finish;
       ++sub;
-      const int c0 = __ldg(g.grp_off + grp);
-      const unsigned cnt = static_cast<unsigned>(__ldg(g.grp_off + grp + 1) - c0) * FPC;
+      // CN phase: every (CN of the group, frame) item; Jacobi within the group
+      const int c0 = __ldg(g.cn_off + grp);
+      const unsigned cnt = static_cast<unsigned>(__ldg(g.cn_off + grp + 1) - c0) * FPC;
       for (unsigned it = tid; it < cnt; it += nt) {
         const unsigned f = it % FPC;
         if (s.done[f]) continue;
-        cn_update<D, EXACT, FPC>(g, s, __ldg(g.grp_cns + c0 + it / FPC), f);
+        cn_update<D, EXACT, FPC>(s, g.cn_rec + static_cast<size_t>(c0 + it / FPC) * cs, f);
       }
       __syncthreads();
-      const int t0 = __ldg(g.touch_off + grp);
-      const unsigned tcnt = static_cast<unsigned>(__ldg(g.touch_off + grp + 1) - t0) * FPC;
+      // VN phase: every (touched VN, frame) item
+      const int t0 = __ldg(g.vn_off + grp);
+      const unsigned tcnt = static_cast<unsigned>(__ldg(g.vn_off + grp + 1) - t0) * FPC;
+      const int4* vrec = reinterpret_cast<const int4*>(g.vn_rec);
       for (unsigned it = tid; it < tcnt; it += nt) {
         const unsigned f = it % FPC;
         if (s.done[f]) continue;
-        vn_refresh<FPC>(g, s, __ldg(g.touch_vns + t0 + it / FPC), f);
+        vn_refresh<FPC, VS>(s, vrec + static_cast<size_t>(t0 + it / FPC) * g.vs4, g.vs4, f);
       }
       __syncthreads();
     }
@@ -223,7 +263,7 @@ __global__ void __launch_bounds__(512) decode_resident(const DevGraph g, const D
       for (unsigned it = tid; it < cnt; it += nt) {
         const unsigned f = it % FPC;
         if (s.done[f]) continue;
-        if (parity<FPC>(g, s, static_cast<int>(it / FPC), f)) atomicAdd(&s.weight[f], 1);
+        if (parity<D, EXACT, FPC>(s, g.all_rec + static_cast<size_t>(it / FPC) * cs, f)) atomicAdd(&s.weight[f], 1);
       }
     }
     __syncthreads();
@@ -329,43 +369,31 @@ __global__ void check_update_kernel(int deg, int64_t rows, const float* __restri
 
 using KernelFn = void (*)(const DevGraph, const DecodeArgs);
 
-template <int D, bool EXACT>
+template <int D, bool EXACT, int VS>
 KernelFn pick_fpc(int fpc) {
   switch (fpc) {
-    case 1: return decode_resident<D, EXACT, 1>;
-    case 2: return decode_resident<D, EXACT, 2>;
-    case 4: return decode_resident<D, EXACT, 4>;
-    case 8: return decode_resident<D, EXACT, 8>;
-    case 16: return decode_resident<D, EXACT, 16>;
+    case 1: return decode_resident<D, EXACT, 1, VS>;
+    case 2: return decode_resident<D, EXACT, 2, VS>;
+    case 4: return decode_resident<D, EXACT, 4, VS>;
+    case 8: return decode_resident<D, EXACT, 8, VS>;
+    case 16: return decode_resident<D, EXACT, 16, VS>;
     default: return nullptr;
   }
 }
 
 KernelFn pick_kernel(const DevGraph& g, int fpc, int* bucket) {
-  if (g.cregular && g.max_cdeg == 6) {
-    *bucket = 6;
-    return pick_fpc<6, true>(fpc);
+  *bucket = cn_bucket(g.max_cdeg, g.cregular);
+  switch (*bucket) {
+    case 6: return g.vs4 == 1 ? pick_fpc<6, true, 1>(fpc) : pick_fpc<6, true, 0>(fpc);
+    case 3: return pick_fpc<3, true, 0>(fpc);
+    case 8: return pick_fpc<8, false, 0>(fpc);
+    case 16: return pick_fpc<16, false, 0>(fpc);
+    case 32: return pick_fpc<32, false, 0>(fpc);
+    default: return nullptr;
   }
-  if (g.cregular && g.max_cdeg == 3) {
-    *bucket = 3;
-    return pick_fpc<3, true>(fpc);
-  }
-  if (g.max_cdeg <= 8) {
-    *bucket = 8;
-    return pick_fpc<8, false>(fpc);
-  }
-  if (g.max_cdeg <= 16) {
-    *bucket = 16;
-    return pick_fpc<16, false>(fpc);
-  }
-  if (g.max_cdeg <= 32) {
-    *bucket = 32;
-    return pick_fpc<32, false>(fpc);
-  }
-  return nullptr;
 }
 
-size_t frame_bytes(const DevGraph& g) { return 4ull * (static_cast<size_t>(g.E) + 2ull * g.n); }
+size_t frame_bytes(const DevGraph& g) { return 4ull * (static_cast<size_t>(g.E) + 1 + 2ull * g.n); }
 
 int device_smem_optin() {
   static std::mutex mu;
@@ -394,18 +422,26 @@ Plan plan_decode(const DevGraph& g, int64_t frames) {
   Plan p;
   const size_t limit = static_cast<size_t>(device_smem_optin()) - 1024;
   const size_t per = frame_bytes(g);
+  auto bytes = [&](int f) { return f * per + 20 * f + 16; };
   int fpc = g_tune_fpc.load();
   if (fpc <= 0) {
     fpc = 8;
-    while (fpc > 1 && fpc * per + 20 * fpc > limit) fpc /= 2;
+    while (fpc > 1 && bytes(fpc) > limit) fpc /= 2;
   }
-  if (fpc * per + 20 * fpc > limit) return p;  // does not fit: no resident plan
+  if (bytes(fpc) > limit) return p;  // does not fit: no resident plan
   int bucket = 0;
   if (!pick_kernel(g, fpc, &bucket)) return p;
+  const int max_nt = bucket <= 8 ? 1024 : 512;
+  int nt = g_tune_threads.load();
+  if (nt <= 0) {
+    // one CN item per thread for the largest group, in whole warps
+    nt = (fpc * g.max_cn_items + 31) / 32 * 32;
+    nt = std::max(128, std::min(nt, max_nt));
+  }
   p.kernel = 1;
   p.fpc = fpc;
-  p.threads = g_tune_threads.load() > 0 ? g_tune_threads.load() : 256;
-  p.smem = static_cast<int>(fpc * per + 20 * fpc);
+  p.threads = std::min(nt, max_nt);
+  p.smem = static_cast<int>(bytes(fpc));
   p.degree_bucket = bucket;
   p.ctas = (frames + fpc - 1) / fpc;
   return p;

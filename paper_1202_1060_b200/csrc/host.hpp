@@ -84,6 +84,24 @@ struct ScheduleData {
   int max_group = 0, max_touched = 0;
 };
 
+// Compact per-group records read by the resident kernel (one vectorised,
+// frame-broadcast load per CN or VN item):
+//   CN record  [edge offset, degree, v_0 .. v_{d-1}, pad]   stride cs ints
+//   VN record  [v, e_0 .. e_{d-1}, E ...]                    stride 4*vs4 ints
+// where E is a c2v slot that is always zero, so short VN records sum +0.
+// A CN listed twice in one group is kept once (its second update would read
+// the same pre-group messages and write the same values).
+struct KernelTables {
+  int cs = 0, vs4 = 0;
+  std::vector<int32_t> cn_off, cn_rec;  // per group; record index offsets
+  std::vector<int32_t> vn_off, vn_rec;
+  std::vector<int32_t> all_rec;         // every CN in index order (syndrome)
+  int max_cn_items = 0, max_vn_items = 0;
+};
+
+// cs = CN record stride in ints (>= 2 + max CN degree, multiple of 4)
+KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs);
+
 ScheduleData schedule_from_groups(const CodeData& c, Kind kind, const Rows& groups);
 ScheduleData flooding_schedule(const CodeData& c);
 ScheduleData reference_random_schedule(const CodeData& c, Kind kind, int G, double overlap, uint64_t seed);

@@ -148,6 +148,48 @@ int iteration_budget(const ScheduleData& s, int n_checks, int i_max) {
   return static_cast<int>(std::floor(static_cast<double>(n_checks) * i_max / (n_checks + extra)));
 }
 
+KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs) {
+  if (c.E >= (1 << 30)) throw std::invalid_argument("code too large for 32-bit edge records");
+  if (cs < 2 + c.max_cdeg || cs % 4) throw std::invalid_argument("bad CN record stride");
+  KernelTables t;
+  t.cs = cs;
+  t.vs4 = (1 + c.max_vdeg + 3) / 4;
+  auto put_cn = [&](std::vector<int32_t>& out, int r) {
+    const int off = c.row_off[r], deg = c.row_off[r + 1] - off;
+    out.push_back(off);
+    out.push_back(deg);
+    for (int k = 0; k < deg; ++k) out.push_back(c.cols[off + k]);
+    for (int k = 2 + deg; k < t.cs; ++k) out.push_back(0);
+  };
+  t.cn_off.assign(1, 0);
+  t.vn_off.assign(1, 0);
+  std::vector<char> in_group(c.m, 0);
+  for (int g = 0; g < s.G; ++g) {
+    int items = 0;
+    for (int i = s.grp_off[g]; i < s.grp_off[g + 1]; ++i) {
+      const int r = s.grp_cns[i];
+      if (in_group[r]) continue;
+      in_group[r] = 1;
+      put_cn(t.cn_rec, r);
+      ++items;
+    }
+    for (int i = s.grp_off[g]; i < s.grp_off[g + 1]; ++i) in_group[s.grp_cns[i]] = 0;
+    t.cn_off.push_back(t.cn_off.back() + items);
+    t.max_cn_items = std::max(t.max_cn_items, items);
+    for (int i = s.touch_off[g]; i < s.touch_off[g + 1]; ++i) {
+      const int v = s.touch_vns[i];
+      t.vn_rec.push_back(v);
+      int w = 1;
+      for (int j = c.var_off[v]; j < c.var_off[v + 1]; ++j, ++w) t.vn_rec.push_back(c.var_edges[j]);
+      for (; w < 4 * t.vs4; ++w) t.vn_rec.push_back(c.E);
+    }
+    t.vn_off.push_back(s.touch_off[g + 1]);
+    t.max_vn_items = std::max(t.max_vn_items, s.touch_off[g + 1] - s.touch_off[g]);
+  }
+  for (int r = 0; r < c.m; ++r) put_cn(t.all_rec, r);
+  return t;
+}
+
 // VNs adjacent to both consecutive groups (schedule.hpp:175-201)
 std::vector<int> measure_cocsg(const CodeData& c, const ScheduleData& s) {
   std::vector<int> out;

@@ -11,14 +11,15 @@ struct DevGraph {
   int max_cdeg = 0, max_vdeg = 0;
   bool cregular = false;  // every CN has degree max_cdeg
   bool vregular = false;  // every VN has degree max_vdeg
-  const int32_t* row_off = nullptr;
-  const int32_t* cols = nullptr;
-  const int32_t* var_off = nullptr;
-  const int32_t* var_edges = nullptr;
-  const int32_t* grp_off = nullptr;
-  const int32_t* grp_cns = nullptr;
-  const int32_t* touch_off = nullptr;
-  const int32_t* touch_vns = nullptr;
+  int cs = 0;   // CN record stride (ints), multiple of 4
+  int vs4 = 0;  // VN record stride (int4 units)
+  int max_cn_items = 0, max_vn_items = 0;
+  const int32_t* cols = nullptr;     // CSR columns (state dumps)
+  const int32_t* cn_off = nullptr;   // [G+1] CN record offsets per group
+  const int32_t* cn_rec = nullptr;   // see host.hpp KernelTables
+  const int32_t* vn_off = nullptr;   // [G+1]
+  const int32_t* vn_rec = nullptr;
+  const int32_t* all_rec = nullptr;  // [m] CN records, syndrome
 };
 
 // One decode launch (all pointers are device pointers; outputs nullable).
@@ -38,6 +39,16 @@ struct DecodeArgs {
   float* c2v_out = nullptr;  // [frames][E] (debug dump)
   float* v2c_out = nullptr;  // [frames][E]
 };
+
+// Degree bucket of the CN kernel instantiation (exact for regular rows).
+inline int cn_bucket(int max_cdeg, bool cregular) {
+  if (cregular && (max_cdeg == 3 || max_cdeg == 6)) return max_cdeg;
+  if (max_cdeg <= 8) return 8;
+  if (max_cdeg <= 16) return 16;
+  if (max_cdeg <= 32) return 32;
+  return 0;
+}
+inline int cn_record_stride(int bucket) { return (2 + bucket + 3) / 4 * 4; }
 
 struct Plan {
   int kernel = 0;  // 1 = SMEM-resident frame-interleaved
