@@ -159,9 +159,13 @@ int make_sched(const std::shared_ptr<CodeImpl>& code, ldpcb::ScheduleData s, ldp
   return LDPCB_OK;
 }
 
-ldpcb::DevGraph dev_graph(ldpcb_code code, ldpcb_schedule s) {
+void check_pair(ldpcb_code code, ldpcb_schedule s) {
   need(code && s, "null handle");
   need(s->impl->code.get() == code->impl.get(), "schedule was built for a different code");
+}
+
+ldpcb::DevGraph dev_graph(ldpcb_code code, ldpcb_schedule s) {
+  check_pair(code, s);
   const auto& c = code->impl->device();
   const auto& d = s->impl->device();
   const auto& h = code->impl->host;
@@ -427,6 +431,7 @@ int ldpcb_decode_device(ldpcb_code code, ldpcb_schedule s, int64_t frames, const
                         int early_stop, uint8_t* d_bits, int bits_packed, int32_t* d_iterations, uint8_t* d_converged,
                         float* d_posterior, int32_t* d_trace, int64_t* d_counters, void* stream) {
   return guard([&] {
+    check_pair(code, s);
     need(max_iters >= 1, "max_iters must be >= 1");
     need(frames >= 0, "frames must be >= 0");
     need(frames == 0 || d_llr != nullptr, "null LLR buffer");
@@ -455,6 +460,7 @@ int ldpcb_decode_host(ldpcb_code code, ldpcb_schedule s, int64_t frames, const f
                       int early_stop, uint8_t* bits, int bits_packed, int32_t* iterations, uint8_t* converged,
                       float* posterior, int64_t* counters) {
   return guard([&] {
+    check_pair(code, s);
     need(max_iters >= 1, "max_iters must be >= 1");
     need(frames >= 0, "frames must be >= 0");
     need(frames == 0 || llr != nullptr, "null LLR buffer");
@@ -544,6 +550,7 @@ int ldpcb_decode_host(ldpcb_code code, ldpcb_schedule s, int64_t frames, const f
 int ldpcb_simulate_device(ldpcb_code code, ldpcb_schedule s, double sigma2, uint64_t channel_seed, int64_t frame_begin,
                           int64_t frames, int max_iters, int early_stop, int64_t* d_counters, void* stream) {
   return guard([&] {
+    check_pair(code, s);
     need(max_iters >= 1, "max_iters must be >= 1");
     need(frames >= 0 && frame_begin >= 0, "bad frame range");
     need(sigma2 > 0.0, "sigma2 must be positive");
@@ -585,6 +592,7 @@ int ldpcb_check_update_device(int degree, int64_t rows, const float* d_v2c, floa
 int ldpcb_run_subiterations_device(ldpcb_code code, ldpcb_schedule s, int64_t frames, const float* d_llr,
                                    int n_subiters, float* d_c2v, float* d_v2c, void* stream) {
   return guard([&] {
+    check_pair(code, s);
     need(n_subiters >= 1, "n_subiters must be >= 1");
     const auto g = dev_graph(code, s);
     ldpcb::DecodeArgs a;

@@ -1,0 +1,372 @@
+"""Parity of the sm_100a decoder (called through the C ABI) with the CPU
+oracle and the reference's golden vectors.
+
+Bars (BASELINE.json north_star): construction / grouping / syndromes
+bit-exact; per-frame hard decisions + iteration counts identical on >= 99.9%
+of frames; posteriors within 1e-3 relative (floor max(|L|,1)) where |L| < 30
+on converged frames; BER/FER inside the reference's 95% CI. Per-message
+checks of the fp32 CN update use |d| <= 1e-4 * max(|ref|, 1)."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+MSG_TOL = 1e-4
+POST_TOL = 1e-3
+THREADS = os.cpu_count() or 8
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return torch
+
+
+def load(name):
+    return np.load(os.path.join(GOLDEN, name + ".npz"))
+
+
+def cu(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def msg_close(got, want, tol=MSG_TOL):
+    got, want = np.asarray(got, np.float64), np.asarray(want, np.float64)
+    err = np.abs(got - want) / np.maximum(np.abs(want), 1.0)
+    return err.max() if err.size else 0.0
+
+
+def frame_parity(gpu, ref):
+    same = (gpu["bits"] == ref["bits"]).all(axis=1) & (gpu["iterations"] == ref["iterations"])
+    same &= gpu["converged"] == ref["converged"]
+    return same
+
+
+def post_stats(gp, rp, mask_frames):
+    rp, gp = rp[mask_frames].astype(np.float64), gp[mask_frames].astype(np.float64)
+    sel = np.abs(rp) < 30
+    err = np.abs(gp - rp)[sel] / np.maximum(np.abs(rp[sel]), 1.0)
+    if err.size == 0:
+        return 1.0, 0.0
+    return float((err <= POST_TOL).mean()), float(err.max())
+
+
+def to_np(out):
+    return {k: v.cpu().numpy() for k, v in out.items()}
+
+
+# ------------------------------------------------------------ CN kernel ----
+def test_check_update_known_answers(P, torch):
+    out = P.check_update(cu(torch, [[1.7, -0.4]])).cpu().numpy()[0]
+    assert out[0] == pytest.approx(-0.4, rel=1e-5) and out[1] == pytest.approx(1.7, rel=1e-5)
+    out = P.check_update(cu(torch, [[2.0, -1.0, 5.0]])).cpu().numpy()[0]
+    assert out[2] == pytest.approx(-0.7353257, abs=1e-4)
+    assert out[2] == pytest.approx(2 * math.atanh(math.tanh(1.0) * math.tanh(-0.5)), rel=1e-5)
+    out = P.check_update(cu(torch, [[3.0, 0.0, -2.0]])).cpu().numpy()[0]
+    assert out[0] == 0.0 and out[2] == 0.0  # exact, decoder.hpp:77-83
+    assert out[1] == pytest.approx(2 * math.atanh(math.tanh(1.5) * math.tanh(-1.0)), rel=1e-5)
+    six = P.check_update(cu(torch, [[3.0, 0.0, -2.0, 1.0, 0.5, 7.0]])).cpu().numpy()[0]
+    assert np.all(np.delete(six, 1) == 0.0)
+
+
+def test_check_update_golden_and_properties(P, torch):
+    z = load("check_update")
+    rng = np.random.default_rng(3)
+    worst = 0.0
+    for d in range(2, 13):
+        idx = np.where(z["deg"] == d)[0]
+        x, want = z["v2c"][idx, :d], z["c2v"][idx, :d]
+        got = P.check_update(cu(torch, x)).cpu().numpy().astype(np.float64)
+        worst = max(worst, msg_close(got, want))
+        xs = x.astype(np.float32).astype(np.float64)
+        sp = np.prod(np.sign(xs), axis=1, keepdims=True)
+        assert np.all(np.sign(got) == sp * np.sign(xs))  # sign rule (test_decoder.cpp:223-229)
+        for k in range(d):  # magnitude rule (:230-235), fp32 slack
+            other = np.min(np.abs(np.delete(xs, k, axis=1)), axis=1)
+            assert np.all(np.abs(got[:, k]) <= other * (1 + 1e-5) + 1e-6)
+        perm = rng.permutation(d)  # permutation invariance (:237-247)
+        gp = P.check_update(cu(torch, x[:, perm])).cpu().numpy()
+        assert msg_close(gp, got[:, perm]) <= 1e-5
+    assert worst <= MSG_TOL, worst
+    print(f"check_update: max |d|/max(|ref|,1) = {worst:.2e} over 2000 reference cases")
+
+
+def test_check_update_saturation(P, torch):
+    x = np.array([[30.0] * 6, [-30.0] + [30.0] * 5, [1e-7] + [25.0] * 5, [40.0] * 2 + [0.5] * 4], np.float32)
+    got = P.check_update(cu(torch, x)).cpu().numpy()
+    for row, g in zip(x, got):
+        want = [2 * math.atanh(np.prod([math.tanh(0.5 * min(max(v, -30), 30)) for j, v in enumerate(row) if j != k]))
+                if True else 0 for k in range(len(row))]
+        want = np.clip(want, -30, 30)
+        assert msg_close(g, want) <= 1e-3
+    assert np.all(np.abs(got) <= 30.0)
+
+
+# ------------------------------------------------------- sub-iterations ----
+def test_forward_flow_and_untouched_vns(P, torch):
+    # test_decoder.cpp:114-127 on the Fig. 1 graph
+    g = P.TannerGraph.from_check_lists(8, [[0, 1, 2], [1, 3, 4], [3, 5, 6], [5, 7]])
+    s = P.GroupSchedule.from_groups(g, P.NONDISJOINT, [[0, 1], [2, 3]])
+    llr = np.array([[0.3, -0.2, 1.0, -1.5, 0.7, 0.1, -0.4, 0.9]], np.float32)
+    c2v, v2c = (t.cpu().numpy()[0] for t in P.run_subiterations(g, s, cu(torch, llr), 1))
+    c2_to_v4 = 2 * math.atanh(math.tanh(0.5 * llr[0, 1]) * math.tanh(0.5 * llr[0, 4]))
+    e = g.var_edge_ids[3][1]
+    assert v2c[e] == pytest.approx(llr[0, 3] + c2_to_v4, rel=1e-5)
+    for e in g.var_edge_ids[5]:
+        assert v2c[e] == llr[0, 5]  # untouched VN keeps its channel value exactly
+    assert np.all(c2v[g.edge_id(2, 0) :] == 0)
+
+
+@pytest.mark.parametrize("sched", ["bp", "ndgsbp", "gsbp"])
+def test_messages_track_reference(P, torch, orc, sched):
+    g = P.configs.c1_code()
+    s = P.configs.c1_schedules(g)[sched]
+    og = orc.graph(g.n_vars, *g.csr())
+    s2 = P.sigma2_from_ebn0(1.5, g.rate)
+    llr = orc.transmit_batch_f32(s2, 3, g.n_vars, 0, 4)
+    for nsub in (1, 2, s.n_groups, s.n_groups + 1):
+        c2v, v2c = (t.cpu().numpy() for t in P.run_subiterations(g, s, cu(torch, llr), nsub))
+        for f in range(len(llr)):
+            rc, rv = orc.run_subiterations(og, s.groups, llr[f].astype(np.float64), nsub)
+            assert msg_close(c2v[f], rc) <= MSG_TOL * (1 + 4 * (nsub > 2)), (sched, nsub, f)
+            assert msg_close(v2c[f], rv) <= MSG_TOL * (1 + 4 * (nsub > 2)), (sched, nsub, f)
+
+
+# ---------------------------------------------------------------- decode ----
+@pytest.mark.parametrize("sched", ["ndgsbp", "gsbp", "bp"])
+@pytest.mark.parametrize("mode", ["es20", "fix10"])
+def test_decode_matches_reference_golden(P, torch, sched, mode):
+    z = load("decode_c1")
+    g = P.configs.c1_code()
+    assert np.array_equal(g.csr()[1], z["c1_cols"])  # same H as the fixture
+    s = P.configs.c1_schedules(g)[sched]
+    es, iters = (True, 20) if mode == "es20" else (False, 10)
+    out = to_np(P.decode_batch(g, s, cu(torch, z["c1_llr"]), iters, early_stop=es, packed=True, posterior=True,
+                               trace=True))
+    assert np.array_equal(out["bits"], z[f"c1_{sched}_{mode}_bits"])
+    assert np.array_equal(out["iterations"], z[f"c1_{sched}_{mode}_iters"])
+    assert np.array_equal(out["converged"], z[f"c1_{sched}_{mode}_conv"])
+    assert np.array_equal(out["syndrome_trace"], z[f"c1_{sched}_{mode}_trace"])
+    frac, worst = post_stats(out["posterior"], z[f"c1_{sched}_{mode}_post"], z[f"c1_{sched}_{mode}_conv"] == 1)
+    assert frac >= 0.999, (frac, worst)
+
+
+@pytest.mark.parametrize("sched", ["ndgsbp", "gsbp", "bp"])
+def test_c1_parity_10k_frames(P, torch, orc, sched):
+    """BASELINE config 1: 10^4 frames, 2.0 dB, <=20 iterations, early stop."""
+    g = P.configs.c1_code()
+    s = P.configs.c1_schedules(g)[sched]
+    og = orc.graph(g.n_vars, *g.csr())
+    s2 = P.sigma2_from_ebn0(2.0, g.rate)
+    F = 10_000
+    llr = orc.transmit_batch_f32(s2, 1, g.n_vars, 0, F, THREADS)
+    gpu = to_np(P.decode_batch(g, s, cu(torch, llr), 20, posterior=True))
+    ref = orc.decode_batch(og, s.groups, llr, 20, early_stop=True, threads=THREADS, posterior=True)
+    same = frame_parity(gpu, ref)
+    frac, worst = post_stats(gpu["posterior"], ref["posterior"], same & (ref["converged"] == 1))
+    fer_g, fer_r = (gpu["bits"].sum(1) > 0).mean(), (ref["bits"].sum(1) > 0).mean()
+    lo, hi = __import__("paper_1202_1060_b200.sim", fromlist=["x"]).clopper_pearson(int(fer_r * F), F)
+    print(f"{sched}: identical {same.mean():.5f}, FER {fer_g:.4f} (ref {fer_r:.4f}, CI [{lo:.4f},{hi:.4f}]), "
+          f"iters {gpu['iterations'].mean():.3f}/{ref['iterations'].mean():.3f}, posteriors within 1e-3: "
+          f"{frac:.6f} (max {worst:.2e})")
+    assert same.mean() >= 0.999
+    assert lo <= fer_g <= hi
+    assert frac >= 0.9999
+
+
+def test_fixed_iterations_and_trace(P, torch, orc):
+    g = P.configs.c1_code()
+    s = P.configs.c1_schedules(g)["ndgsbp"]
+    og = orc.graph(g.n_vars, *g.csr())
+    s2 = P.sigma2_from_ebn0(1.5, g.rate)
+    llr = orc.transmit_batch_f32(s2, 9, g.n_vars, 0, 500, THREADS)
+    gpu = to_np(P.decode_batch(g, s, cu(torch, llr), 10, early_stop=False, trace=True))
+    assert np.all(gpu["iterations"] == 10)
+    ref = orc.decode_batch(og, s.groups, llr, 10, early_stop=False, threads=THREADS, trace=True)
+    same = frame_parity(gpu, ref)
+    assert same.mean() >= 0.999
+    assert np.array_equal(gpu["syndrome_trace"][same], ref["syndrome_trace"][same])
+    # converged <=> zero syndrome at the last iteration
+    assert np.array_equal(gpu["converged"] == 1, gpu["syndrome_trace"][:, -1] == 0)
+
+
+def test_syndrome_is_exact_on_output_bits(P, torch, orc):
+    g = P.configs.c1_code()
+    s = P.configs.c1_schedules(g)["gsbp"]
+    llr = orc.transmit_batch_f32(P.sigma2_from_ebn0(1.25, g.rate), 5, g.n_vars, 0, 2000, THREADS)
+    out = to_np(P.decode_batch(g, s, cu(torch, llr), 20, trace=True))
+    rows = np.array(g.check_adj)
+    syn = np.bitwise_xor.reduce(out["bits"][:, rows], axis=2).sum(1)
+    last = out["syndrome_trace"][np.arange(len(llr)), out["iterations"] - 1]
+    assert np.array_equal(syn, last)
+    assert np.all(syn[out["converged"] == 1] == 0) and np.all(syn[out["converged"] == 0] > 0)
+
+
+def test_device_channel_bit_exact(P, torch, orc):
+    for n, ebn0, seed, f0 in ((1008, 2.0, 1, 0), (1001, 0.5, 7, 12345), (64, 4.0, 99, 2**33)):
+        s2 = P.sigma2_from_ebn0(ebn0, 0.5)
+        d = P.transmit_all_zero(n, s2, seed, f0, 300).cpu().numpy()
+        h = orc.transmit_batch_f32(s2, seed, n, f0, 300, THREADS)
+        assert np.array_equal(d, h), (n, np.abs(d - h).max())
+
+
+def test_simulate_counters_match_oracle(P, torch, corc):
+    g = P.configs.c1_code()
+    s = P.configs.c1_schedules(g)["ndgsbp"]
+    og = corc.graph(g.n_vars, *g.csr())
+    s2 = P.sigma2_from_ebn0(1.75, g.rate)
+    gpu = P.simulate(g, s, s2, 11, 1000, 3000, 20).cpu().numpy()
+    ref = corc.simulate(og, s.groups, s2, 11, 1000, 3000, 20, threads=THREADS)
+    assert gpu[0] == ref[0] == 3000
+    assert abs(int(gpu[2]) - int(ref[2])) <= 3  # frame errors: <= 0.1% of frames may differ
+    assert abs(int(gpu[4]) - int(ref[4])) <= 3 * 20
+
+
+def test_counters_agree_with_outputs(P, torch, orc):
+    g = P.configs.c1_code()
+    s = P.configs.c1_schedules(g)["bp"]
+    llr = orc.transmit_batch_f32(P.sigma2_from_ebn0(1.5, g.rate), 2, g.n_vars, 0, 777, THREADS)
+    cnt = torch.zeros(6, dtype=torch.int64, device="cuda")
+    out = to_np(P.decode_batch(g, s, cu(torch, llr), 20, counters=cnt))
+    be = out["bits"].sum(1)
+    want = [777, be.sum(), (be > 0).sum(), out["converged"].sum(), out["iterations"].sum(),
+            out["iterations"][out["converged"] == 1].sum()]
+    assert cnt.cpu().tolist() == [int(x) for x in want]
+
+
+@pytest.mark.parametrize("fpc,threads", [(1, 96), (2, 0), (4, 512), (8, 0), (8, 256)])
+def test_tuning_and_ragged_batches_are_identical(P, torch, orc, fpc, threads):
+    g = P.configs.c1_code()
+    s = P.configs.c1_schedules(g)["ndgsbp"]
+    llr = cu(torch, orc.transmit_batch_f32(P.sigma2_from_ebn0(1.5, g.rate), 4, g.n_vars, 0, 37, THREADS))
+    P.set_tuning(0, 0)
+    base = to_np(P.decode_batch(g, s, llr, 20, posterior=True))
+    try:
+        P.set_tuning(fpc, threads)
+        other = to_np(P.decode_batch(g, s, llr, 20, posterior=True))
+        for k in base:
+            assert np.array_equal(base[k], other[k]), k
+        for F in (1, 3, 13):  # tails smaller than a CTA
+            part = to_np(P.decode_batch(g, s, llr[:F].contiguous(), 20, posterior=True))
+            for k in part:
+                assert np.array_equal(part[k], base[k][:F]), (F, k)
+    finally:
+        P.set_tuning(0, 0)
+
+
+def test_empty_batch_and_bad_arguments(P, torch):
+    g = P.configs.c1_code()
+    s = P.configs.c1_schedules(g)["ndgsbp"]
+    out = P.decode_batch(g, s, torch.empty((0, g.n_vars), dtype=torch.float32, device="cuda"), 5)
+    assert out["iterations"].numel() == 0
+    with pytest.raises(ValueError):
+        P.decode_batch(g, s, torch.zeros((2, 7), dtype=torch.float32, device="cuda"), 5)
+    with pytest.raises(ValueError):
+        P.decode_batch(g, s, torch.zeros((2, g.n_vars), dtype=torch.float32, device="cuda"), 0)
+
+
+def test_host_api_equals_device_api(P, torch, orc):
+    g = P.configs.c1_code()
+    s = P.configs.c1_schedules(g)["ndgsbp"]
+    llr = orc.transmit_batch_f32(P.sigma2_from_ebn0(2.0, g.rate), 1, g.n_vars, 0, 1000, THREADS)
+    dev = to_np(P.decode_batch(g, s, cu(torch, llr), 10, early_stop=False, packed=True))
+    bits = np.empty_like(dev["bits"])
+    its = np.empty(1000, np.int32)
+    cv = np.empty(1000, np.uint8)
+    cnt = np.zeros(6, np.int64)
+    P.decode_host(g, s, llr, 10, early_stop=False, packed=True, bits=bits, iterations=its, converged=cv, counters=cnt)
+    assert np.array_equal(bits, dev["bits"]) and np.array_equal(its, dev["iterations"])
+    assert np.array_equal(cv, dev["converged"]) and cnt[0] == 1000
+
+
+def test_reference_single_frame_api(P, torch):
+    # test_decoder.cpp:149-168
+    g = P.TannerGraph.random_regular(60, 3, 6, 21)
+    out = P.decode(g, P.make_flooding_schedule(g), np.full(60, 1e9), 10)
+    assert out.converged and out.iterations == 1 and not out.bits.any()
+    fig1 = P.TannerGraph.from_check_lists(8, [[0, 1, 2], [1, 3, 4], [3, 5, 6], [5, 7]])
+    word = np.array([1, 1, 0, 1, 0, 1, 0, 1], np.uint8)
+    out = P.decode(fig1, P.make_flooding_schedule(fig1), np.where(word == 1, -30.0, 30.0), 5)
+    assert out.converged and out.iterations == 1 and np.array_equal(out.bits, word)
+    assert out.syndrome_weight_trace == [0] and out.cn_updates == 4
+    with pytest.raises(ValueError):
+        P.decode(g, P.make_flooding_schedule(g), np.zeros(59), 10)
+    with pytest.raises(ValueError):
+        P.decode(g, P.make_flooding_schedule(g), np.zeros(60), 0)
+
+
+def test_r0_nondisjoint_is_identical_to_disjoint(P, torch, orc):
+    g = P.TannerGraph.random_regular(60, 3, 6, 11)
+    gs = P.make_disjoint_schedule(g, 5, 401)
+    nd = P.make_nondisjoint_schedule(g, 5, 0.0, 401)
+    assert gs.groups == nd.groups
+    llr = cu(torch, orc.transmit_batch_f32(P.sigma2_from_ebn0(1.5, g.rate), 17, 60, 0, 64))
+    a = to_np(P.decode_batch(g, gs, llr, 40, trace=True, posterior=True))
+    b = to_np(P.decode_batch(g, nd, llr, 40, trace=True, posterior=True))
+    for k in a:
+        assert np.array_equal(a[k], b[k])
+
+
+def test_determinism(P, torch, orc):
+    g = P.configs.c1_code()
+    s = P.configs.c1_schedules(g)["ndgsbp"]
+    llr = cu(torch, orc.transmit_batch_f32(P.sigma2_from_ebn0(1.0, g.rate), 8, g.n_vars, 0, 999, THREADS))
+    a = to_np(P.decode_batch(g, s, llr, 20, posterior=True, trace=True))
+    b = to_np(P.decode_batch(g, s, llr, 20, posterior=True, trace=True))
+    for k in a:
+        assert np.array_equal(a[k], b[k])
+
+
+def _parity(P, torch, orc, g, s, ebn0, iters, F, seed=1):
+    og = orc.graph(g.n_vars, *g.csr())
+    llr = orc.transmit_batch_f32(P.sigma2_from_ebn0(ebn0, g.rate), seed, g.n_vars, 0, F, THREADS)
+    gpu = to_np(P.decode_batch(g, s, cu(torch, llr), iters, posterior=True))
+    ref = orc.decode_batch(og, s.groups, llr, iters, early_stop=True, threads=THREADS, posterior=True)
+    same = frame_parity(gpu, ref)
+    frac, worst = post_stats(gpu["posterior"], ref["posterior"], same & (ref["converged"] == 1))
+    return same.mean(), frac, worst, gpu
+
+
+@pytest.mark.parametrize("sched", ["ndgsbp", "gsbp"])
+def test_qc_code_parity(P, torch, orc, sched):
+    """BASELINE config 3 code and grouping (n=1944, irregular rows <= 16)."""
+    g = P.configs.c3_code()
+    s = P.configs.c3_schedules(g)[sched]
+    same, frac, worst, gpu = _parity(P, torch, orc, g, s, 2.0, 15, 2000)
+    print(f"QC {sched}: identical {same:.5f}, posteriors within 1e-3 {frac:.6f} (max {worst:.2e})")
+    assert same >= 0.999 and frac >= 0.9999
+
+
+def test_irregular_code_parity(P, torch, orc):
+    """VN degrees {2,3,8} (BASELINE config 4 ensemble) at n=2400: multi-int4
+    VN records and zero-slot padding."""
+    g = P.TannerGraph.irregular(2400, [2, 3, 8], [1200, 960, 240], 6, 5)
+    s = P.GroupSchedule.windows(g, 5, 300, 240)
+    same, frac, worst, _ = _parity(P, torch, orc, g, s, 1.5, 30, 1000)
+    print(f"irregular: identical {same:.5f}, posteriors within 1e-3 {frac:.6f} (max {worst:.2e})")
+    assert same >= 0.999 and frac >= 0.9999
+
+
+def test_random_reference_schedules_parity(P, torch, orc):
+    """The reference's own random groupings (make_nondisjoint_schedule) on the
+    shipped-size (504,252) code."""
+    g = P.TannerGraph.random_regular(504, 3, 6, 3)
+    for s in (P.make_nondisjoint_schedule(g, 12, 0.4, 123), P.make_disjoint_schedule(g, 12, 17)):
+        same, frac, _, _ = _parity(P, torch, orc, g, s, 2.0, 50, 1000)
+        assert same >= 0.999 and frac >= 0.9999
+
+
+def test_kernel_launches_counted(P, torch):
+    g = P.configs.c1_code()
+    s = P.configs.c1_schedules(g)["ndgsbp"]
+    before = P.kernel_launches()
+    P.decode_batch(g, s, torch.zeros((8, g.n_vars), dtype=torch.float32, device="cuda"), 2)
+    torch.cuda.synchronize()
+    assert P.kernel_launches() == before + 1
