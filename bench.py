@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU sample duration")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--fpc", type=int, default=0, help="frames per CTA (0 = library plan)")
+    ap.add_argument("--threads", type=int, default=0, help="threads per CTA (0 = library plan)")
     return ap.parse_args()
 
 
@@ -204,6 +206,7 @@ def run_b200(args):
 
     g, s, ebn0, desc = workload(args.workload)
     sigma2 = mean_sigma2(P, g, ebn0)
+    P.set_tuning(args.fpc, args.threads)
     B = args.frames
     n = g.n_vars
     K = n - g.n_checks

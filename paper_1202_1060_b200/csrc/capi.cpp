@@ -102,7 +102,7 @@ struct SchedImpl {
   ldpcb::KernelTables tables;
   std::mutex mu;
   struct Dev {
-    int32_t *cn_off, *cn_rec, *vn_off, *vn_rec, *all_rec;
+    int32_t *cn_off, *cn_rec, *fix_off, *fix_rec, *all_vn_rec, *all_rec, *edge_slot;
     std::vector<void*> ptrs;
   };
   std::map<int, Dev> dev;
@@ -119,10 +119,12 @@ struct SchedImpl {
     Dev x;
     x.cn_off = upload(tables.cn_off);
     x.cn_rec = upload(tables.cn_rec);
-    x.vn_off = upload(tables.vn_off);
-    x.vn_rec = upload(tables.vn_rec);
+    x.fix_off = upload(tables.fix_off);
+    x.fix_rec = upload(tables.fix_rec);
+    x.all_vn_rec = upload(tables.all_vn_rec);
     x.all_rec = upload(tables.all_rec);
-    x.ptrs = {x.cn_off, x.cn_rec, x.vn_off, x.vn_rec, x.all_rec};
+    x.edge_slot = upload(tables.edge_slot);
+    x.ptrs = {x.cn_off, x.cn_rec, x.fix_off, x.fix_rec, x.all_vn_rec, x.all_rec, x.edge_slot};
     return dev.emplace(d, std::move(x)).first->second;
   }
 };
@@ -154,7 +156,8 @@ int make_sched(const std::shared_ptr<CodeImpl>& code, ldpcb::ScheduleData s, ldp
   impl->code = code;
   impl->host = std::move(s);
   const int bucket = ldpcb::cn_bucket(code->host.max_cdeg, code->cregular);
-  if (bucket > 0) impl->tables = ldpcb::kernel_tables(code->host, impl->host, ldpcb::cn_record_stride(bucket));
+  if (bucket > 0)
+    impl->tables = ldpcb::kernel_tables(code->host, impl->host, ldpcb::cn_record_stride(bucket), code->cregular);
   *out = new ldpcb_schedule_s{impl};
   return LDPCB_OK;
 }
@@ -182,13 +185,17 @@ ldpcb::DevGraph dev_graph(ldpcb_code code, ldpcb_schedule s) {
   if (t.cs == 0) throw std::runtime_error("check-node degree above 32 is not supported by the resident kernel");
   g.cs = t.cs;
   g.vs4 = t.vs4;
+  g.n_slots = t.n_slots;
+  g.recompute = t.recompute;
   g.max_cn_items = t.max_cn_items;
-  g.max_vn_items = t.max_vn_items;
+  g.max_fix_items = t.max_fix_items;
   g.cols = c.cols;
+  g.edge_slot = d.edge_slot;
   g.cn_off = d.cn_off;
   g.cn_rec = d.cn_rec;
-  g.vn_off = d.vn_off;
-  g.vn_rec = d.vn_rec;
+  g.fix_off = d.fix_off;
+  g.fix_rec = d.fix_rec;
+  g.all_vn_rec = d.all_vn_rec;
   g.all_rec = d.all_rec;
   return g;
 }

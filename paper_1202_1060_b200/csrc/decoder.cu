@@ -58,32 +58,35 @@ __device__ __forceinline__ float mufu_lg2(float x) {
 
 __device__ __forceinline__ float clamp_llr(float x) { return fminf(fmaxf(x, -kClamp), kClamp); }
 
-// Exclusion boxplus over one CN. x[k] are the clamped incoming v2c for
-// k < deg (EXACT: deg == D); store(k, c2v_k) receives every output.
+// Exclusion boxplus over one CN. x[k] are the incoming v2c for k < deg
+// (EXACT: deg == D); |v2c| is clamped to 30 here (decoder.hpp:125) and the
+// sign travels in the IEEE sign bit. store(k, c2v_k) receives every output.
+//
+// Exactly-zero inputs: ex2(-0) = 1 exactly, and every combine below is
+// symmetric under N <-> D of an operand equal to (a, a), so any output whose
+// exclusion set holds a zero ends with N == D bit-for-bit and a magnitude of
+// exactly 0 (decoder.hpp:77-83) without per-edge bookkeeping.
 template <int D, bool EXACT, class Store>
 __device__ __forceinline__ void boxplus_row(const float (&x)[D], int deg, Store&& store) {
   float z[D];
-  unsigned sg = 0, zr = 0;
+  unsigned sg = 0;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     if (EXACT || k < deg) {
-      sg |= static_cast<unsigned>(x[k] < 0.f) << k;
-      zr |= static_cast<unsigned>(x[k] == 0.f) << k;
-      z[k] = mufu_ex2(fabsf(x[k]) * -kLog2e);
+      sg ^= __float_as_uint(x[k]);
+      z[k] = mufu_ex2(fminf(fabsf(x[k]), kClamp) * -kLog2e);
     } else {
       z[k] = 0.f;  // boxplus identity (N, D) = (0, 1)
     }
   }
-  const unsigned par = __popc(sg) & 1u;
   auto emit = [&](int k, float num, float den) {
     if (EXACT || k < deg) {
-      float mag = fminf((mufu_lg2(den) - mufu_lg2(num)) * kLn2, kClamp);
-      if (zr & ~(1u << k)) mag = 0.f;
-      const unsigned s = par ^ ((sg >> k) & 1u);
-      store(k, s ? -mag : mag);
+      const float mag = fminf(fabsf(mufu_lg2(den) - mufu_lg2(num)) * kLn2, kClamp);
+      const unsigned sgn = (sg ^ __float_as_uint(x[k])) & 0x80000000u;
+      store(k, __uint_as_float(__float_as_uint(mag) | sgn));
     }
   };
-  // prefix products p[k] = z0 (+) ... (+) zk, k <= D-2
+  // prefix p[k] = z0 (+) ... (+) zk for k <= D-2: (N, D) <- (N + z D, D + z N)
   float pn[D > 1 ? D - 1 : 1], pd[D > 1 ? D - 1 : 1];
   pn[0] = z[0];
   pd[0] = 1.f;
@@ -96,7 +99,9 @@ __device__ __forceinline__ void boxplus_row(const float (&x)[D], int deg, Store&
   float sn = z[D - 1], sd = 1.f;  // suffix s[k+1]
 #pragma unroll
   for (int k = D - 2; k >= 1; --k) {
-    emit(k, fmaf(pn[k - 1], sd, sn * pd[k - 1]), fmaf(pd[k - 1], sd, pn[k - 1] * sn));
+    // out_k = p[k-1] (+) s[k+1], rounded symmetrically (see above)
+    emit(k, __fadd_rn(__fmul_rn(pn[k - 1], sd), __fmul_rn(sn, pd[k - 1])),
+         __fadd_rn(__fmul_rn(pd[k - 1], sd), __fmul_rn(pn[k - 1], sn)));
     const float tn = fmaf(z[k], sd, sn);
     const float td = fmaf(z[k], sn, sd);
     sn = tn;
@@ -105,19 +110,8 @@ __device__ __forceinline__ void boxplus_row(const float (&x)[D], int deg, Store&
   emit(0, sn, sd);
 }
 
-struct Shared {
-  float* c2v;  // [(E+1)][FPC]; slot E stays zero (pads short VN records)
-  float* P;    // [n][FPC] posterior (channel + all c2v), unclamped
-  float* L;    // [n][FPC] clamped channel LLR
-  int* done;   // [FPC]
-  int* weight;
-  int* iters;
-  int* conv;
-  int* berr;
-};
-
-// One CN record (host.hpp KernelTables) -> the clamped incoming messages
-// v2c = clamp(P_v - c2v_e) (posterior form of var_update, decoder.hpp:91-105).
+// One CN record (host.hpp KernelTables): [slot of edge 0, single-touch
+// mask, v_0 ... v_{D-1}] (v = -1 past the degree).
 template <int D, bool EXACT>
 struct CnRecord {
   static constexpr int kInts = (2 + D + 3) / 4 * 4;
@@ -133,101 +127,147 @@ struct CnRecord {
       r[4 * i + 3] = t.w;
     }
   }
-  __device__ __forceinline__ int off() const { return r[0]; }
-  __device__ __forceinline__ int deg() const { return EXACT ? D : r[1]; }
+  __device__ __forceinline__ int slot() const { return r[0]; }
+  __device__ __forceinline__ unsigned mask() const { return static_cast<unsigned>(r[1]); }
   __device__ __forceinline__ int var(int k) const { return r[2 + k]; }
+  __device__ __forceinline__ bool has(int k) const { return EXACT || r[2 + k] >= 0; }
+  __device__ __forceinline__ int deg() const {
+    if (EXACT) return D;
+    int d = 0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) d += r[2 + k] >= 0;
+    return d;
+  }
 };
 
+// Frame-interleaved shared-memory views of ONE frame: element i of a per-slot
+// or per-VN array lives at base[i * FPC].
+//   c2v : [n_slots] check-to-variable messages (last slot stays zero)
+//   P   : [n]       posterior = channel + all c2v (unclamped)
+//   L   : [n]       clamped channel LLR
+// v2c is never stored: v2c = clamp(P_v - c2v_e), the posterior form of
+// var_update (decoder.hpp:91-105). A VN touched by only this CN of the group
+// (mask bit) gets its posterior updated in place, P += c2v_new - c2v_old:
+// no other CN of the group reads it, so the Jacobi order of
+// decoder.hpp:107-113 is kept.
 template <int D, bool EXACT, int FPC>
-__device__ __forceinline__ void cn_update(const Shared& s, const int32_t* __restrict__ rec, unsigned f) {
+__device__ __forceinline__ void cn_update(float* __restrict__ c2v, float* __restrict__ P,
+                                          const int32_t* __restrict__ rec) {
   const CnRecord<D, EXACT> cr(rec);
-  const int off = cr.off(), deg = cr.deg();
-  float x[D];
+  const int base = cr.slot();
+  const unsigned mask = cr.mask();
+  float x[D], pv[D], old[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) {
-    x[k] = 0.f;
-    if (EXACT || k < deg) x[k] = clamp_llr(s.P[cr.var(k) * FPC + f] - s.c2v[(off + k) * FPC + f]);
+    x[k] = pv[k] = old[k] = 0.f;
+    if (cr.has(k)) {
+      pv[k] = P[cr.var(k) * FPC];
+      old[k] = c2v[(base + k) * FPC];
+      x[k] = pv[k] - old[k];
+    }
   }
-  boxplus_row<D, EXACT>(x, deg, [&](int k, float c) { s.c2v[(off + k) * FPC + f] = c; });
+  boxplus_row<D, EXACT>(x, cr.deg(), [&](int k, float c) {
+    c2v[(base + k) * FPC] = c;
+    if (mask & (1u << k)) P[cr.var(k) * FPC] = pv[k] + (c - old[k]);
+  });
 }
 
-// P_v = L_v + sum of c2v over the VN's edges in ascending-CN order (the
-// totals of decoder.hpp:162-165; refreshes every v2c of v at once).
+// P_v = L_v + sum of c2v over the VN's edges in ascending-CN order: the
+// totals of decoder.hpp:162-165 (and every v2c of v refreshed at once).
 template <int FPC, int VS>
-__device__ __forceinline__ void vn_refresh(const Shared& s, const int4* __restrict__ rec, int vs4, unsigned f) {
+__device__ __forceinline__ void vn_sum(const float* __restrict__ c2v, float* __restrict__ P,
+                                       const float* __restrict__ L, const int4* __restrict__ rec, int vs4) {
   int4 t = __ldg(rec);
   const int v = t.x;
-  float acc = s.L[v * FPC + f];
-  acc += s.c2v[t.y * FPC + f];
-  acc += s.c2v[t.z * FPC + f];
-  acc += s.c2v[t.w * FPC + f];
+  float acc = L[v * FPC] + c2v[t.y * FPC];
+  acc += c2v[t.z * FPC];
+  acc += c2v[t.w * FPC];
   const int nq = VS > 0 ? VS : vs4;
 #pragma unroll
   for (int q = 1; q < nq; ++q) {
     t = __ldg(rec + q);
-    acc += s.c2v[t.x * FPC + f];
-    acc += s.c2v[t.y * FPC + f];
-    acc += s.c2v[t.z * FPC + f];
-    acc += s.c2v[t.w * FPC + f];
+    acc += c2v[t.x * FPC];
+    acc += c2v[t.y * FPC];
+    acc += c2v[t.z * FPC];
+    acc += c2v[t.w * FPC];
   }
-  s.P[v * FPC + f] = acc;
+  P[v * FPC] = acc;
+}
+
+// Two independent VN records per step so their loads overlap.
+template <int FPC, int VS>
+__device__ __forceinline__ void vn_sum_range(const float* __restrict__ c2v, float* __restrict__ P,
+                                             const float* __restrict__ L, const int4* __restrict__ rec, int vs4,
+                                             int j0, int count, int jstep) {
+  int j = j0;
+  for (; j + jstep < count; j += 2 * jstep) {
+    vn_sum<FPC, VS>(c2v, P, L, rec + j * vs4, vs4);
+    vn_sum<FPC, VS>(c2v, P, L, rec + (j + jstep) * vs4, vs4);
+  }
+  if (j < count) vn_sum<FPC, VS>(c2v, P, L, rec + j * vs4, vs4);
 }
 
 template <int D, bool EXACT, int FPC>
-__device__ __forceinline__ unsigned parity(const Shared& s, const int32_t* __restrict__ rec, unsigned f) {
+__device__ __forceinline__ int parity(const float* __restrict__ P, const int32_t* __restrict__ rec) {
   const CnRecord<D, EXACT> cr(rec);
   unsigned p = 0;
 #pragma unroll
   for (int k = 0; k < D; ++k)
-    if (EXACT || k < cr.deg()) p ^= static_cast<unsigned>(s.P[cr.var(k) * FPC + f] < 0.f);
-  return p;
+    if (cr.has(k)) p ^= static_cast<unsigned>(P[cr.var(k) * FPC] < 0.f);
+  return static_cast<int>(p);
 }
 
-constexpr int max_threads_for(int D) { return D <= 8 ? 1024 : 512; }
+constexpr int max_threads_for(int D) { return D <= 6 ? 1024 : (D <= 16 ? 512 : 256); }
 
+// Each thread serves one frame (f = tid % FPC, blockDim a multiple of 32 and
+// FPC | 32) and walks the items of that frame with stride blockDim / FPC.
 template <int D, bool EXACT, int FPC, int VS>
-__global__ void __launch_bounds__(max_threads_for(D)) decode_resident(const DevGraph g, const DecodeArgs a) {
+__global__ void __launch_bounds__(max_threads_for(D), 1) decode_resident(const DevGraph g, const DecodeArgs a) {
+  constexpr int CS = CnRecord<D, EXACT>::kInts;
   extern __shared__ __align__(16) float smem[];
   __shared__ int s_active;
   const int tid = threadIdx.x, nt = blockDim.x;
-  const int n = g.n, E = g.E, cs = g.cs;
-  Shared s;
-  s.c2v = smem;
-  s.P = s.c2v + static_cast<size_t>(E + 1) * FPC;
-  s.L = s.P + static_cast<size_t>(n) * FPC;
-  s.done = reinterpret_cast<int*>(s.L + static_cast<size_t>(n) * FPC);
-  s.weight = s.done + FPC;
-  s.iters = s.weight + FPC;
-  s.conv = s.iters + FPC;
-  s.berr = s.conv + FPC;
+  const int n = g.n, m = g.m, S = g.n_slots;
+  const int vs4 = VS > 0 ? VS : g.vs4;
+  const int f = tid % FPC, j0 = tid / FPC, jstep = nt / FPC;
+  float* const c2v = smem + f;
+  float* const P = smem + S * FPC + f;
+  float* const L = P + n * FPC;
+  int* const s_done = reinterpret_cast<int*>(smem + (S + 2 * n) * FPC);
+  int* const s_weight = s_done + FPC;
+  int* const s_iters = s_weight + FPC;
+  int* const s_conv = s_iters + FPC;
+  int* const s_berr = s_conv + FPC;
+  const int4* const all_vn = reinterpret_cast<const int4*>(g.all_vn_rec);
 
   const int64_t f0 = static_cast<int64_t>(blockIdx.x) * FPC;
   const int nf = static_cast<int>(min(static_cast<int64_t>(FPC), a.frames - f0));
 
   // ---- prologue: init_state (decoder.hpp:39-52) in posterior form
-  const float* llr = a.llr + f0 * n;
-  for (int i = tid; i < nf * n; i += nt) {
-    const int f = i / n, v = i - f * n;
-    const float x = clamp_llr(__ldg(llr + i));
-    s.L[v * FPC + f] = x;
-    s.P[v * FPC + f] = x;
-  }
   {
-    const int total = (E + 1) * FPC;
-    float4* c4 = reinterpret_cast<float4*>(s.c2v);
+    const float* llr = a.llr + f0 * n;
+    for (int i = tid; i < nf * n; i += nt) {
+      const int ff = i / n, v = i - ff * n;
+      const float x = clamp_llr(__ldg(llr + i));
+      smem[(S + v) * FPC + ff] = x;
+      smem[(S + n + v) * FPC + ff] = x;
+    }
+    const int total = S * FPC;
+    float4* c4 = reinterpret_cast<float4*>(smem);
     for (int i = tid; i < total / 4; i += nt) c4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int i = total / 4 * 4 + tid; i < total; i += nt) s.c2v[i] = 0.f;
+    for (int i = total / 4 * 4 + tid; i < total; i += nt) smem[i] = 0.f;
   }
   if (tid < FPC) {
-    s.done[tid] = tid >= nf;
-    s.weight[tid] = 0;
-    s.iters[tid] = 0;
-    s.conv[tid] = 0;
-    s.berr[tid] = 0;
+    s_done[tid] = tid >= nf;
+    s_weight[tid] = 0;
+    s_iters[tid] = 0;
+    s_conv[tid] = 0;
+    s_berr[tid] = 0;
   }
   if (a.trace)
     for (int i = tid; i < nf * a.max_iters; i += nt) a.trace[f0 * a.max_iters + i] = -1;
   __syncthreads();
+  bool live = f < nf;
 
   const bool dump = a.max_subiters > 0;
   int sub = 0;
@@ -235,112 +275,115 @@ __global__ void __launch_bounds__(max_threads_for(D)) decode_resident(const DevG
     for (int grp = 0; grp < g.G; ++grp) {
       if (dump && sub == a.max_subiters) goto finish;
       ++sub;
-      // CN phase: every (CN of the group, frame) item; Jacobi within the group
-      const int c0 = __ldg(g.cn_off + grp);
-      const unsigned cnt = static_cast<unsigned>(__ldg(g.cn_off + grp + 1) - c0) * FPC;
-      for (unsigned it = tid; it < cnt; it += nt) {
-        const unsigned f = it % FPC;
-        if (s.done[f]) continue;
-        cn_update<D, EXACT, FPC>(s, g.cn_rec + static_cast<size_t>(c0 + it / FPC) * cs, f);
+      // CN phase: every (CN of the group, frame); Jacobi within the group
+      const int c0 = __ldg(g.cn_off + grp), cn = __ldg(g.cn_off + grp + 1) - c0;
+      if (live) {
+        const int32_t* rec = g.cn_rec + static_cast<size_t>(c0) * CS;
+        for (int j = j0; j < cn; j += jstep) cn_update<D, EXACT, FPC>(c2v, P, rec + j * CS);
       }
       __syncthreads();
-      // VN phase: every (touched VN, frame) item
-      const int t0 = __ldg(g.vn_off + grp);
-      const unsigned tcnt = static_cast<unsigned>(__ldg(g.vn_off + grp + 1) - t0) * FPC;
-      const int4* vrec = reinterpret_cast<const int4*>(g.vn_rec);
-      for (unsigned it = tid; it < tcnt; it += nt) {
-        const unsigned f = it % FPC;
-        if (s.done[f]) continue;
-        vn_refresh<FPC, VS>(s, vrec + static_cast<size_t>(t0 + it / FPC) * g.vs4, g.vs4, f);
+      // VNs shared by two or more CNs of the group: exact re-sum
+      const int x0 = __ldg(g.fix_off + grp), xn = __ldg(g.fix_off + grp + 1) - x0;
+      if (xn > 0) {
+        if (live)
+          vn_sum_range<FPC, VS>(c2v, P, L, reinterpret_cast<const int4*>(g.fix_rec) + static_cast<size_t>(x0) * vs4,
+                                vs4, j0, xn, jstep);
+        __syncthreads();
       }
-      __syncthreads();
     }
     if (dump) continue;
+    // ---- exact totals once per iteration (decoder.hpp:162-165); this also
+    // removes the rounding of the in-place posterior updates
+    if (g.recompute) {
+      if (live) vn_sum_range<FPC, VS>(c2v, P, L, all_vn, vs4, j0, n, jstep);
+      __syncthreads();
+    }
     if (!(a.early_stop || a.trace || iter == a.max_iters)) continue;
     // ---- hard decision + syndrome weight (decoder.hpp:166-171)
-    {
-      const unsigned cnt = static_cast<unsigned>(g.m) * FPC;
-      for (unsigned it = tid; it < cnt; it += nt) {
-        const unsigned f = it % FPC;
-        if (s.done[f]) continue;
-        if (parity<D, EXACT, FPC>(s, g.all_rec + static_cast<size_t>(it / FPC) * cs, f)) atomicAdd(&s.weight[f], 1);
-      }
+    if (live) {
+      int w = 0;
+      for (int j = j0; j < m; j += jstep) w += parity<D, EXACT, FPC>(P, g.all_rec + j * CS);
+      if (w) atomicAdd(&s_weight[f], w);
     }
     __syncthreads();
     if (tid == 0) {
       int active = 0;
-      for (int f = 0; f < nf; ++f) {
-        if (s.done[f]) continue;
-        const int w = s.weight[f];
-        if (a.trace) a.trace[(f0 + f) * a.max_iters + iter - 1] = w;
-        s.iters[f] = iter;
-        s.conv[f] = w == 0;
-        s.weight[f] = 0;
+      for (int ff = 0; ff < nf; ++ff) {
+        if (s_done[ff]) continue;
+        const int w = s_weight[ff];
+        if (a.trace) a.trace[(f0 + ff) * a.max_iters + iter - 1] = w;
+        s_iters[ff] = iter;
+        s_conv[ff] = w == 0;
+        s_weight[ff] = 0;
         if (w == 0 && a.early_stop)
-          s.done[f] = 1;  // decoder.hpp:173-177
+          s_done[ff] = 1;  // decoder.hpp:173-177
         else
           ++active;
       }
       s_active = active;
     }
     __syncthreads();
+    live = !s_done[f];
     if (s_active == 0) break;
   }
 finish:
   __syncthreads();
   if (dump) {
-    for (int i = tid; i < nf * E; i += nt) {
-      const int f = i / E, e = i - f * E;
-      const float c = s.c2v[e * FPC + f];
-      if (a.c2v_out) a.c2v_out[f0 * E + i] = c;
-      if (a.v2c_out) a.v2c_out[f0 * E + i] = clamp_llr(s.P[__ldg(g.cols + e) * FPC + f] - c);
+    if (g.recompute && f < nf) vn_sum_range<FPC, VS>(c2v, P, L, all_vn, vs4, j0, n, jstep);
+    __syncthreads();
+    if (f < nf) {
+      const int E = g.E;
+      for (int e = j0; e < E; e += jstep) {
+        const float c = c2v[__ldg(g.edge_slot + e) * FPC];
+        if (a.c2v_out) a.c2v_out[(f0 + f) * E + e] = c;
+        if (a.v2c_out) a.v2c_out[(f0 + f) * E + e] = clamp_llr(P[__ldg(g.cols + e) * FPC] - c);
+      }
     }
     return;
   }
-  // ---- epilogue: hard decisions, error counts
-  if (a.bits && a.bits_packed) {
-    const int nb = (n + 7) >> 3;
-    for (int i = tid; i < nb * FPC; i += nt) {
-      const int f = i % FPC, b = i / FPC;
-      if (f >= nf) continue;
-      unsigned byte = 0;
+  // ---- epilogue: hard decisions (tie -> 0, decoder.hpp:166), error counts
+  if (f < nf) {
+    int errs = 0;
+    if (a.bits && a.bits_packed) {
+      const int nb = (n + 7) >> 3;
+      uint8_t* out = a.bits + (f0 + f) * nb;
+      for (int b = j0; b < nb; b += jstep) {
+        unsigned byte = 0;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int v = b * 8 + j;
-        if (v < n && s.P[v * FPC + f] < 0.f) byte |= 1u << j;
+        for (int j = 0; j < 8; ++j) {
+          const int v = b * 8 + j;
+          if (v < n && P[v * FPC] < 0.f) byte |= 1u << j;
+        }
+        out[b] = static_cast<uint8_t>(byte);
+        errs += __popc(byte);
       }
-      a.bits[(f0 + f) * nb + b] = static_cast<uint8_t>(byte);
-      if (byte) atomicAdd(&s.berr[f], __popc(byte));
+    } else if (a.bits || a.counters) {
+      for (int v = j0; v < n; v += jstep) {
+        const int bit = P[v * FPC] < 0.f;
+        if (a.bits) a.bits[(f0 + f) * n + v] = static_cast<uint8_t>(bit);
+        errs += bit;
+      }
     }
-  } else if (a.bits || a.counters) {
-    for (int i = tid; i < nf * n; i += nt) {
-      const int f = i / n, v = i - f * n;
-      const int bit = s.P[v * FPC + f] < 0.f;  // tie -> 0 (decoder.hpp:166)
-      if (a.bits) a.bits[f0 * n + i] = static_cast<uint8_t>(bit);
-      if (bit) atomicAdd(&s.berr[f], 1);
-    }
+    if (errs) atomicAdd(&s_berr[f], errs);
+    if (a.posterior)
+      for (int v = j0; v < n; v += jstep) a.posterior[(f0 + f) * n + v] = P[v * FPC];
   }
-  if (a.posterior)
-    for (int i = tid; i < nf * n; i += nt) {
-      const int f = i / n, v = i - f * n;
-      a.posterior[f0 * n + i] = s.P[v * FPC + f];
-    }
   if (tid < nf) {
-    const int it = a.early_stop ? s.iters[tid] : a.max_iters;
+    const int it = a.early_stop ? s_iters[tid] : a.max_iters;
     if (a.iterations) a.iterations[f0 + tid] = it;
-    if (a.converged) a.converged[f0 + tid] = static_cast<uint8_t>(s.conv[tid]);
+    if (a.converged) a.converged[f0 + tid] = static_cast<uint8_t>(s_conv[tid]);
   }
   __syncthreads();
   if (tid == 0 && a.counters) {
     unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
-    for (int f = 0; f < nf; ++f) {
-      const int it = a.early_stop ? s.iters[f] : a.max_iters;
+    for (int ff = 0; ff < nf; ++ff) {
+      const int it = a.early_stop ? s_iters[ff] : a.max_iters;
       c[0] += 1;
-      c[1] += s.berr[f];
-      c[2] += s.berr[f] > 0;
-      c[3] += s.conv[f];
+      c[1] += s_berr[ff];
+      c[2] += s_berr[ff] > 0;
+      c[3] += s_conv[ff];
       c[4] += it;
-      c[5] += s.conv[f] ? it : 0;
+      c[5] += s_conv[ff] ? it : 0;
     }
     for (int i = 0; i < 6; ++i) atomicAdd(a.counters + i, c[i]);
   }
@@ -363,7 +406,7 @@ __global__ void check_update_kernel(int deg, int64_t rows, const float* __restri
   if (r >= rows) return;
   float x[D];
 #pragma unroll
-  for (int k = 0; k < D; ++k) x[k] = (EXACT || k < deg) ? clamp_llr(v2c[r * deg + k]) : 0.f;
+  for (int k = 0; k < D; ++k) x[k] = (EXACT || k < deg) ? v2c[r * deg + k] : 0.f;
   boxplus_row<D, EXACT>(x, deg, [&](int k, float c) { c2v[r * deg + k] = c; });
 }
 
@@ -393,7 +436,14 @@ KernelFn pick_kernel(const DevGraph& g, int fpc, int* bucket) {
   }
 }
 
-size_t frame_bytes(const DevGraph& g) { return 4ull * (static_cast<size_t>(g.E) + 1 + 2ull * g.n); }
+size_t frame_bytes(const DevGraph& g) { return 4ull * (static_cast<size_t>(g.n_slots) + 2ull * g.n); }
+
+int device_smem_per_sm() {
+  int dev = 0, v = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev) != cudaSuccess) v = 228 * 1024;
+  return v;
+}
 
 int device_smem_optin() {
   static std::mutex mu;
@@ -425,18 +475,22 @@ Plan plan_decode(const DevGraph& g, int64_t frames) {
   auto bytes = [&](int f) { return f * per + 20 * f + 16; };
   int fpc = g_tune_fpc.load();
   if (fpc <= 0) {
+    // largest FPC that still lets two CTAs share an SM (their barriers and
+    // latencies overlap); else the largest that fits at all
+    const size_t sm_bytes = static_cast<size_t>(device_smem_per_sm()) - 2048;
     fpc = 8;
-    while (fpc > 1 && bytes(fpc) > limit) fpc /= 2;
+    while (fpc > 1 && (bytes(fpc) > limit || 2 * bytes(fpc) > sm_bytes)) fpc /= 2;
+    if (bytes(fpc) > limit || 2 * bytes(fpc) > sm_bytes) fpc = 1;
   }
   if (bytes(fpc) > limit) return p;  // does not fit: no resident plan
   int bucket = 0;
   if (!pick_kernel(g, fpc, &bucket)) return p;
-  const int max_nt = bucket <= 8 ? 1024 : 512;
+  const int max_nt = bucket <= 6 ? 1024 : (bucket <= 16 ? 512 : 256);
   int nt = g_tune_threads.load();
   if (nt <= 0) {
     // one CN item per thread for the largest group, in whole warps
     nt = (fpc * g.max_cn_items + 31) / 32 * 32;
-    nt = std::max(128, std::min(nt, max_nt));
+    nt = std::max(128, std::min(nt, std::min(max_nt, 512)));
   }
   p.kernel = 1;
   p.fpc = fpc;

@@ -85,22 +85,32 @@ struct ScheduleData {
 };
 
 // Compact per-group records read by the resident kernel (one vectorised,
-// frame-broadcast load per CN or VN item):
-//   CN record  [edge offset, degree, v_0 .. v_{d-1}, pad]   stride cs ints
-//   VN record  [v, e_0 .. e_{d-1}, E ...]                    stride 4*vs4 ints
-// where E is a c2v slot that is always zero, so short VN records sum +0.
+// frame-broadcast load per CN or VN item). c2v lives in "slots": for
+// check-regular codes slot(m, k) = m * slot_stride + k with an ODD stride, so
+// the consecutive CNs of a window hit distinct shared-memory banks; otherwise
+// slot = CN-major edge id. The last slot is always zero (pads VN records).
+//   CN record  [slot of edge 0, single-touch mask, v_0 .. v_{d-1}, -1 ...]  cs ints
+//   VN record  [v, slot_0 .. slot_{d-1} (ascending CN), zero slot ...]    4*vs4 ints
+// Bit k of the mask is set when v_k has no other CN in the group: the CN
+// thread then updates that VN's posterior in place; VNs shared by two or more
+// CNs of the group ("fix" records) are re-summed after the CN phase.
 // A CN listed twice in one group is kept once (its second update would read
 // the same pre-group messages and write the same values).
 struct KernelTables {
   int cs = 0, vs4 = 0;
-  std::vector<int32_t> cn_off, cn_rec;  // per group; record index offsets
-  std::vector<int32_t> vn_off, vn_rec;
-  std::vector<int32_t> all_rec;         // every CN in index order (syndrome)
-  int max_cn_items = 0, max_vn_items = 0;
+  int slot_stride = 0;     // 0: slot = edge id
+  int n_slots = 0;         // including the zero slot
+  bool recompute = false;  // some CN updates a posterior in place
+  std::vector<int32_t> cn_off, cn_rec;    // per group
+  std::vector<int32_t> fix_off, fix_rec;  // per group: VNs shared by >= 2 CNs
+  std::vector<int32_t> all_vn_rec;        // every VN (exact totals, decoder.hpp:162-165)
+  std::vector<int32_t> all_rec;           // every CN in index order (syndrome)
+  std::vector<int32_t> edge_slot;         // CN-major edge id -> slot
+  int max_cn_items = 0, max_fix_items = 0;
 };
 
 // cs = CN record stride in ints (>= 2 + max CN degree, multiple of 4)
-KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs);
+KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, bool regular_rows);
 
 ScheduleData schedule_from_groups(const CodeData& c, Kind kind, const Rows& groups);
 ScheduleData flooding_schedule(const CodeData& c);

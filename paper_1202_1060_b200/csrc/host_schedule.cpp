@@ -148,45 +148,77 @@ int iteration_budget(const ScheduleData& s, int n_checks, int i_max) {
   return static_cast<int>(std::floor(static_cast<double>(n_checks) * i_max / (n_checks + extra)));
 }
 
-KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs) {
-  if (c.E >= (1 << 30)) throw std::invalid_argument("code too large for 32-bit edge records");
+KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, bool regular_rows) {
   if (cs < 2 + c.max_cdeg || cs % 4) throw std::invalid_argument("bad CN record stride");
   KernelTables t;
   t.cs = cs;
   t.vs4 = (1 + c.max_vdeg + 3) / 4;
-  auto put_cn = [&](std::vector<int32_t>& out, int r) {
+  t.slot_stride = regular_rows ? (c.max_cdeg | 1) : 0;
+  const long long slots = (t.slot_stride ? static_cast<long long>(c.m) * t.slot_stride : c.E) + 1;
+  if (slots >= (1ll << 30)) throw std::invalid_argument("code too large for 32-bit edge records");
+  t.n_slots = static_cast<int>(slots);
+  const int zero = t.n_slots - 1;
+  t.edge_slot.resize(c.E);
+  for (int r = 0; r < c.m; ++r)
+    for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e)
+      t.edge_slot[e] = t.slot_stride ? r * t.slot_stride + (e - c.row_off[r]) : e;
+  auto put_vn = [&](std::vector<int32_t>& out, int v) {
+    out.push_back(v);
+    int w = 1;
+    for (int j = c.var_off[v]; j < c.var_off[v + 1]; ++j, ++w) out.push_back(t.edge_slot[c.var_edges[j]]);
+    for (; w < 4 * t.vs4; ++w) out.push_back(zero);
+  };
+  auto put_cn = [&](std::vector<int32_t>& out, int r, uint32_t mask) {
     const int off = c.row_off[r], deg = c.row_off[r + 1] - off;
-    out.push_back(off);
-    out.push_back(deg);
+    out.push_back(t.edge_slot[off]);
+    out.push_back(static_cast<int32_t>(mask));
     for (int k = 0; k < deg; ++k) out.push_back(c.cols[off + k]);
-    for (int k = 2 + deg; k < t.cs; ++k) out.push_back(0);
+    for (int k = 2 + deg; k < t.cs; ++k) out.push_back(-1);
   };
   t.cn_off.assign(1, 0);
-  t.vn_off.assign(1, 0);
+  t.fix_off.assign(1, 0);
   std::vector<char> in_group(c.m, 0);
+  std::vector<int> touches(c.n, 0);
+  std::vector<int> cns, shared_vns;
   for (int g = 0; g < s.G; ++g) {
-    int items = 0;
+    cns.clear();
     for (int i = s.grp_off[g]; i < s.grp_off[g + 1]; ++i) {
       const int r = s.grp_cns[i];
       if (in_group[r]) continue;
       in_group[r] = 1;
-      put_cn(t.cn_rec, r);
-      ++items;
+      cns.push_back(r);
     }
-    for (int i = s.grp_off[g]; i < s.grp_off[g + 1]; ++i) in_group[s.grp_cns[i]] = 0;
-    t.cn_off.push_back(t.cn_off.back() + items);
-    t.max_cn_items = std::max(t.max_cn_items, items);
-    for (int i = s.touch_off[g]; i < s.touch_off[g + 1]; ++i) {
-      const int v = s.touch_vns[i];
-      t.vn_rec.push_back(v);
-      int w = 1;
-      for (int j = c.var_off[v]; j < c.var_off[v + 1]; ++j, ++w) t.vn_rec.push_back(c.var_edges[j]);
-      for (; w < 4 * t.vs4; ++w) t.vn_rec.push_back(c.E);
+    for (int r : cns) {
+      in_group[r] = 0;
+      for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e) ++touches[c.cols[e]];
     }
-    t.vn_off.push_back(s.touch_off[g + 1]);
-    t.max_vn_items = std::max(t.max_vn_items, s.touch_off[g + 1] - s.touch_off[g]);
+    for (int r : cns) {
+      uint32_t mask = 0;
+      for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e)
+        if (touches[c.cols[e]] == 1) mask |= 1u << (e - c.row_off[r]);
+      t.recompute |= mask != 0;
+      put_cn(t.cn_rec, r, mask);
+    }
+    shared_vns.clear();
+    for (int r : cns)
+      for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e) {
+        const int v = c.cols[e];
+        if (touches[v] >= 2) {
+          shared_vns.push_back(v);
+          touches[v] = -touches[v];  // list once
+        }
+      }
+    for (int r : cns)
+      for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e) touches[c.cols[e]] = 0;
+    std::sort(shared_vns.begin(), shared_vns.end());
+    for (int v : shared_vns) put_vn(t.fix_rec, v);
+    t.cn_off.push_back(t.cn_off.back() + static_cast<int>(cns.size()));
+    t.fix_off.push_back(t.fix_off.back() + static_cast<int>(shared_vns.size()));
+    t.max_cn_items = std::max(t.max_cn_items, static_cast<int>(cns.size()));
+    t.max_fix_items = std::max(t.max_fix_items, static_cast<int>(shared_vns.size()));
   }
-  for (int r = 0; r < c.m; ++r) put_cn(t.all_rec, r);
+  for (int v = 0; v < c.n; ++v) put_vn(t.all_vn_rec, v);
+  for (int r = 0; r < c.m; ++r) put_cn(t.all_rec, r, 0);
   return t;
 }
 

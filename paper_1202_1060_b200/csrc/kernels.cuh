@@ -13,13 +13,17 @@ struct DevGraph {
   bool vregular = false;  // every VN has degree max_vdeg
   int cs = 0;   // CN record stride (ints), multiple of 4
   int vs4 = 0;  // VN record stride (int4 units)
-  int max_cn_items = 0, max_vn_items = 0;
-  const int32_t* cols = nullptr;     // CSR columns (state dumps)
-  const int32_t* cn_off = nullptr;   // [G+1] CN record offsets per group
-  const int32_t* cn_rec = nullptr;   // see host.hpp KernelTables
-  const int32_t* vn_off = nullptr;   // [G+1]
-  const int32_t* vn_rec = nullptr;
-  const int32_t* all_rec = nullptr;  // [m] CN records, syndrome
+  int n_slots = 0;         // c2v slots per frame, incl. the zero slot
+  bool recompute = false;  // exact-totals pass needed each iteration
+  int max_cn_items = 0, max_fix_items = 0;
+  const int32_t* cols = nullptr;        // CSR columns (state dumps)
+  const int32_t* edge_slot = nullptr;   // edge id -> c2v slot (state dumps)
+  const int32_t* cn_off = nullptr;      // [G+1] CN record offsets per group
+  const int32_t* cn_rec = nullptr;      // see host.hpp KernelTables
+  const int32_t* fix_off = nullptr;     // [G+1]
+  const int32_t* fix_rec = nullptr;
+  const int32_t* all_vn_rec = nullptr;  // [n] VN records
+  const int32_t* all_rec = nullptr;     // [m] CN records, syndrome
 };
 
 // One decode launch (all pointers are device pointers; outputs nullable).

@@ -1,7 +1,7 @@
 #!/bin/bash
 # One GPU call: bench, launch list, one full ncu capture of the decode kernel.
 set -x
-SMALL="python bench.py --frames 65536 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
+SMALL="python bench.py --frames 65536 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e ${SMALL_ARGS}"
 python bench.py --steps 5 --warmup 3 ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err
 tail -2 gpurun_out/bench.err
 cat gpurun_out/bench.json

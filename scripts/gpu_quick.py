@@ -28,7 +28,7 @@ s = P.configs.c1_schedules(g)['ndgsbp']
 F = 1 << 18
 x = P.transmit_all_zero(g.n_vars, sigma2, 1, 0, F)
 cnt = torch.zeros(6, dtype=torch.int64, device='cuda')
-for fpc, th in [(0,0),(8,512),(8,1024),(4,256),(4,352),(4,512),(2,192),(2,256),(1,96),(1,128)]:
+for fpc, th in [(0,0),(8,672),(8,1024),(4,256),(4,352),(4,512),(4,672),(2,256),(2,512),(1,128)]:
     P.set_tuning(fpc, th)
     for _ in range(2): P.decode_batch(g, s, x, 10, early_stop=False, packed=True)
     torch.cuda.synchronize()
