@@ -143,6 +143,10 @@ int ldpcb_decode_plan(ldpcb_code code, ldpcb_schedule s, int64_t frames, int32_t
                       int32_t *threads, int32_t *smem_bytes, int32_t *degree_bucket);
 /* 0 = automatic */
 int ldpcb_set_tuning(int frames_per_cta, int threads);
+/* 1 (default): in iterations that do not test the syndrome, skip the exact
+ * re-summation of the posteriors (in-place updates carry them); the totals
+ * are exact whenever hard decisions are taken. 0: every iteration. */
+int ldpcb_set_lazy_totals(int on);
 /* number of CUDA kernels this library has launched (process lifetime) */
 int64_t ldpcb_kernel_launches(void);
 

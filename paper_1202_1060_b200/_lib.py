@@ -69,6 +69,7 @@ _SIGS = {
     "ldpcb_decode_plan": (C.c_int, [vp, vp, i64, P32, P32, P32, P32, P32]),
     "ldpcb_set_tuning": (C.c_int, [C.c_int, C.c_int]),
     "ldpcb_kernel_launches": (i64, []),
+    "ldpcb_set_lazy_totals": (C.c_int, [C.c_int]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

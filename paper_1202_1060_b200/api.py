@@ -496,5 +496,9 @@ def set_tuning(frames_per_cta: int = 0, threads: int = 0) -> None:
     check(lib.ldpcb_set_tuning(frames_per_cta, threads))
 
 
+def set_lazy_totals(on: bool) -> None:
+    check(lib.ldpcb_set_lazy_totals(int(on)))
+
+
 def kernel_launches() -> int:
     return int(lib.ldpcb_kernel_launches())

@@ -646,4 +646,11 @@ int ldpcb_set_tuning(int frames_per_cta, int threads) {
 
 int64_t ldpcb_kernel_launches(void) { return ldpcb::kernel_launch_count(); }
 
+int ldpcb_set_lazy_totals(int on) {
+  return guard([&] {
+    ldpcb::set_lazy_totals(on != 0);
+    return LDPCB_OK;
+  });
+}
+
 }  // extern "C"

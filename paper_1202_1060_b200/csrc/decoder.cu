@@ -41,9 +41,12 @@ namespace {
 constexpr float kClamp = 30.0f;  // decoder.hpp:18
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.69314718055994531f;
+// Inside the kernels messages are kept in log2 units (LLR * log2 e), so the
+// boxplus needs no scaling around ex2 / lg2; the clamp scales with them.
+constexpr float kClampB = 43.280851226668897f;  // 30 * log2(e)
 
 std::atomic<int64_t> g_launches{0};
-std::atomic<int> g_tune_fpc{0}, g_tune_threads{0};
+std::atomic<int> g_tune_fpc{0}, g_tune_threads{0}, g_lazy_totals{1};
 
 __device__ __forceinline__ float mufu_ex2(float x) {
   float y;
@@ -57,10 +60,12 @@ __device__ __forceinline__ float mufu_lg2(float x) {
 }
 
 __device__ __forceinline__ float clamp_llr(float x) { return fminf(fmaxf(x, -kClamp), kClamp); }
+__device__ __forceinline__ float clamp_bits(float x) { return fminf(fmaxf(x, -kClampB), kClampB); }
 
-// Exclusion boxplus over one CN. x[k] are the incoming v2c for k < deg
-// (EXACT: deg == D); |v2c| is clamped to 30 here (decoder.hpp:125) and the
-// sign travels in the IEEE sign bit. store(k, c2v_k) receives every output.
+// Exclusion boxplus over one CN, in log2 units. x[k] are the incoming v2c
+// for k < deg (EXACT: deg == D); |v2c| is clamped to 30 nats here
+// (decoder.hpp:125) and the sign travels in the IEEE sign bit.
+// store(k, c2v_k) receives every output, clamped to 30 nats (decoder.hpp:74).
 //
 // Exactly-zero inputs: ex2(-0) = 1 exactly, and every combine below is
 // symmetric under N <-> D of an operand equal to (a, a), so any output whose
@@ -74,14 +79,14 @@ __device__ __forceinline__ void boxplus_row(const float (&x)[D], int deg, Store&
   for (int k = 0; k < D; ++k) {
     if (EXACT || k < deg) {
       sg ^= __float_as_uint(x[k]);
-      z[k] = mufu_ex2(fminf(fabsf(x[k]), kClamp) * -kLog2e);
+      z[k] = mufu_ex2(-fminf(fabsf(x[k]), kClampB));
     } else {
       z[k] = 0.f;  // boxplus identity (N, D) = (0, 1)
     }
   }
   auto emit = [&](int k, float num, float den) {
     if (EXACT || k < deg) {
-      const float mag = fminf(fabsf(mufu_lg2(den) - mufu_lg2(num)) * kLn2, kClamp);
+      const float mag = fminf(fabsf(mufu_lg2(den) - mufu_lg2(num)), kClampB);
       const unsigned sgn = (sg ^ __float_as_uint(x[k])) & 0x80000000u;
       store(k, __uint_as_float(__float_as_uint(mag) | sgn));
     }
@@ -97,8 +102,16 @@ __device__ __forceinline__ void boxplus_row(const float (&x)[D], int deg, Store&
   }
   emit(D - 1, pn[D - 2], pd[D - 2]);
   float sn = z[D - 1], sd = 1.f;  // suffix s[k+1]
+  if (D >= 3) {  // first middle output, suffix = (z[D-1], 1): same rounding pattern without the * 1
+    constexpr int k = D >= 3 ? D - 2 : 1;
+    emit(k, __fadd_rn(pn[k - 1], __fmul_rn(sn, pd[k - 1])), __fadd_rn(pd[k - 1], __fmul_rn(pn[k - 1], sn)));
+    const float tn = z[k] + sn;
+    const float td = fmaf(z[k], sn, 1.f);
+    sn = tn;
+    sd = td;
+  }
 #pragma unroll
-  for (int k = D - 2; k >= 1; --k) {
+  for (int k = D - 3; k >= 1; --k) {
     // out_k = p[k-1] (+) s[k+1], rounded symmetrically (see above)
     emit(k, __fadd_rn(__fmul_rn(pn[k - 1], sd), __fmul_rn(sn, pd[k - 1])),
          __fadd_rn(__fmul_rn(pd[k - 1], sd), __fmul_rn(pn[k - 1], sn)));
@@ -248,7 +261,7 @@ __global__ void __launch_bounds__(max_threads_for(D), 1) decode_resident(const D
     const float* llr = a.llr + f0 * n;
     for (int i = tid; i < nf * n; i += nt) {
       const int ff = i / n, v = i - ff * n;
-      const float x = clamp_llr(__ldg(llr + i));
+      const float x = clamp_llr(__ldg(llr + i)) * kLog2e;
       smem[(S + v) * FPC + ff] = x;
       smem[(S + n + v) * FPC + ff] = x;
     }
@@ -294,11 +307,12 @@ __global__ void __launch_bounds__(max_threads_for(D), 1) decode_resident(const D
     if (dump) continue;
     // ---- exact totals once per iteration (decoder.hpp:162-165); this also
     // removes the rounding of the in-place posterior updates
-    if (g.recompute) {
+    const bool check = a.early_stop || a.trace || iter == a.max_iters;
+    if (g.recompute && (check || !a.lazy_totals)) {
       if (live) vn_sum_range<FPC, VS>(c2v, P, L, all_vn, vs4, j0, n, jstep);
       __syncthreads();
     }
-    if (!(a.early_stop || a.trace || iter == a.max_iters)) continue;
+    if (!check) continue;
     // ---- hard decision + syndrome weight (decoder.hpp:166-171)
     if (live) {
       int w = 0;
@@ -335,8 +349,8 @@ finish:
       const int E = g.E;
       for (int e = j0; e < E; e += jstep) {
         const float c = c2v[__ldg(g.edge_slot + e) * FPC];
-        if (a.c2v_out) a.c2v_out[(f0 + f) * E + e] = c;
-        if (a.v2c_out) a.v2c_out[(f0 + f) * E + e] = clamp_llr(P[__ldg(g.cols + e) * FPC] - c);
+        if (a.c2v_out) a.c2v_out[(f0 + f) * E + e] = c * kLn2;
+        if (a.v2c_out) a.v2c_out[(f0 + f) * E + e] = clamp_bits(P[__ldg(g.cols + e) * FPC] - c) * kLn2;
       }
     }
     return;
@@ -366,7 +380,7 @@ finish:
     }
     if (errs) atomicAdd(&s_berr[f], errs);
     if (a.posterior)
-      for (int v = j0; v < n; v += jstep) a.posterior[(f0 + f) * n + v] = P[v * FPC];
+      for (int v = j0; v < n; v += jstep) a.posterior[(f0 + f) * n + v] = P[v * FPC] * kLn2;
   }
   if (tid < nf) {
     const int it = a.early_stop ? s_iters[tid] : a.max_iters;
@@ -406,8 +420,8 @@ __global__ void check_update_kernel(int deg, int64_t rows, const float* __restri
   if (r >= rows) return;
   float x[D];
 #pragma unroll
-  for (int k = 0; k < D; ++k) x[k] = (EXACT || k < deg) ? v2c[r * deg + k] : 0.f;
-  boxplus_row<D, EXACT>(x, deg, [&](int k, float c) { c2v[r * deg + k] = c; });
+  for (int k = 0; k < D; ++k) x[k] = (EXACT || k < deg) ? v2c[r * deg + k] * kLog2e : 0.f;
+  boxplus_row<D, EXACT>(x, deg, [&](int k, float c) { c2v[r * deg + k] = c * kLn2; });
 }
 
 using KernelFn = void (*)(const DevGraph, const DecodeArgs);
@@ -468,6 +482,9 @@ void set_tuning(int fpc, int threads) {
 
 int64_t kernel_launch_count() { return g_launches.load(); }
 
+void set_lazy_totals(int on) { g_lazy_totals = on; }
+int lazy_totals() { return g_lazy_totals.load(); }
+
 Plan plan_decode(const DevGraph& g, int64_t frames) {
   Plan p;
   const size_t limit = static_cast<size_t>(device_smem_optin()) - 1024;
@@ -501,7 +518,9 @@ Plan plan_decode(const DevGraph& g, int64_t frames) {
   return p;
 }
 
-int launch_decode(const DevGraph& g, const DecodeArgs& a, void* stream, Plan* used) {
+int launch_decode(const DevGraph& g, const DecodeArgs& a_in, void* stream, Plan* used) {
+  DecodeArgs a = a_in;
+  a.lazy_totals = g_lazy_totals.load();
   const Plan p = plan_decode(g, a.frames);
   if (used) *used = p;
   if (p.kernel == 0) return static_cast<int>(cudaErrorInvalidConfiguration);

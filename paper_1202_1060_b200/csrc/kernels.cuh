@@ -33,6 +33,7 @@ struct DecodeArgs {
   int max_iters = 1;
   int early_stop = 1;
   int max_subiters = 0;  // >0: stop after this many sub-iterations and dump state
+  int lazy_totals = 0;   // 1: exact totals only in iterations that test the syndrome
   uint8_t* bits = nullptr;
   int bits_packed = 0;
   int32_t* iterations = nullptr;
@@ -70,6 +71,8 @@ int launch_channel(int n, double sigma2, uint64_t seed, int64_t frame0, int64_t 
 int launch_check_update(int degree, int64_t rows, const float* v2c, float* c2v, void* stream);
 
 void set_tuning(int fpc, int threads);
+void set_lazy_totals(int on);
+int lazy_totals();
 int64_t kernel_launch_count();
 
 }  // namespace ldpcb
