@@ -637,8 +637,8 @@ int ldpcb_set_tuning(int frames_per_cta, int threads) {
     need(frames_per_cta == 0 || frames_per_cta == 1 || frames_per_cta == 2 || frames_per_cta == 4 ||
              frames_per_cta == 8 || frames_per_cta == 16,
          "frames_per_cta must be 0 (auto) or a power of two <= 16");
-    need(threads == 0 || (threads >= 32 && threads <= 1024 && threads % 32 == 0),
-         "threads must be 0 (auto) or a multiple of 32 in [32, 1024]");
+    need(threads == 0 || (threads >= 32 && threads <= 512 && threads % 32 == 0),
+         "threads must be 0 (auto) or a multiple of 32 in [32, 512]");
     ldpcb::set_tuning(frames_per_cta, threads);
     return LDPCB_OK;
   });

@@ -129,7 +129,9 @@ template <int D, bool EXACT>
 struct CnRecord {
   static constexpr int kInts = (2 + D + 3) / 4 * 4;
   int r[kInts];
-  __device__ __forceinline__ explicit CnRecord(const int32_t* __restrict__ p) {
+  CnRecord() = default;
+  __device__ __forceinline__ explicit CnRecord(const int32_t* __restrict__ p) { load(p); }
+  __device__ __forceinline__ void load(const int32_t* __restrict__ p) {
     const int4* q = reinterpret_cast<const int4*>(p);
 #pragma unroll
     for (int i = 0; i < kInts / 4; ++i) {
@@ -165,8 +167,7 @@ struct CnRecord {
 // decoder.hpp:107-113 is kept.
 template <int D, bool EXACT, int FPC>
 __device__ __forceinline__ void cn_update(float* __restrict__ c2v, float* __restrict__ P,
-                                          const int32_t* __restrict__ rec) {
-  const CnRecord<D, EXACT> cr(rec);
+                                          const CnRecord<D, EXACT>& cr) {
   const int base = cr.slot();
   const unsigned mask = cr.mask();
   float x[D], pv[D], old[D];
@@ -189,8 +190,8 @@ __device__ __forceinline__ void cn_update(float* __restrict__ c2v, float* __rest
 // totals of decoder.hpp:162-165 (and every v2c of v refreshed at once).
 template <int FPC, int VS>
 __device__ __forceinline__ void vn_sum(const float* __restrict__ c2v, float* __restrict__ P,
-                                       const float* __restrict__ L, const int4* __restrict__ rec, int vs4) {
-  int4 t = __ldg(rec);
+                                       const float* __restrict__ L, const int4* __restrict__ rec, int vs4,
+                                       int4 t) {
   const int v = t.x;
   float acc = L[v * FPC] + c2v[t.y * FPC];
   acc += c2v[t.z * FPC];
@@ -214,10 +215,11 @@ __device__ __forceinline__ void vn_sum_range(const float* __restrict__ c2v, floa
                                              int j0, int count, int jstep) {
   int j = j0;
   for (; j + jstep < count; j += 2 * jstep) {
-    vn_sum<FPC, VS>(c2v, P, L, rec + j * vs4, vs4);
-    vn_sum<FPC, VS>(c2v, P, L, rec + (j + jstep) * vs4, vs4);
+    const int4 a = __ldg(rec + j * vs4), b = __ldg(rec + (j + jstep) * vs4);
+    vn_sum<FPC, VS>(c2v, P, L, rec + j * vs4, vs4, a);
+    vn_sum<FPC, VS>(c2v, P, L, rec + (j + jstep) * vs4, vs4, b);
   }
-  if (j < count) vn_sum<FPC, VS>(c2v, P, L, rec + j * vs4, vs4);
+  if (j < count) vn_sum<FPC, VS>(c2v, P, L, rec + j * vs4, vs4, __ldg(rec + j * vs4));
 }
 
 template <int D, bool EXACT, int FPC>
@@ -230,12 +232,12 @@ __device__ __forceinline__ int parity(const float* __restrict__ P, const int32_t
   return static_cast<int>(p);
 }
 
-constexpr int max_threads_for(int D) { return D <= 6 ? 1024 : (D <= 16 ? 512 : 256); }
+constexpr int max_threads_for(int D) { return D <= 8 ? 512 : (D <= 16 ? 256 : 128); }
 
 // Each thread serves one frame (f = tid % FPC, blockDim a multiple of 32 and
 // FPC | 32) and walks the items of that frame with stride blockDim / FPC.
 template <int D, bool EXACT, int FPC, int VS>
-__global__ void __launch_bounds__(max_threads_for(D), 1) decode_resident(const DevGraph g, const DecodeArgs a) {
+__global__ void __launch_bounds__(max_threads_for(D), D <= 8 ? 2 : 1) decode_resident(const DevGraph g, const DecodeArgs a) {
   constexpr int CS = CnRecord<D, EXACT>::kInts;
   extern __shared__ __align__(16) float smem[];
   __shared__ int s_active;
@@ -251,7 +253,10 @@ __global__ void __launch_bounds__(max_threads_for(D), 1) decode_resident(const D
   int* const s_iters = s_weight + FPC;
   int* const s_conv = s_iters + FPC;
   int* const s_berr = s_conv + FPC;
+  int* const s_cn_off = s_berr + FPC;       // [G+1] staged group tables
+  int* const s_fix_off = s_cn_off + g.G + 1;  // [G+1]
   const int4* const all_vn = reinterpret_cast<const int4*>(g.all_vn_rec);
+  const int4* const fix_vn = reinterpret_cast<const int4*>(g.fix_rec);
 
   const int64_t f0 = static_cast<int64_t>(blockIdx.x) * FPC;
   const int nf = static_cast<int>(min(static_cast<int64_t>(FPC), a.frames - f0));
@@ -277,10 +282,18 @@ __global__ void __launch_bounds__(max_threads_for(D), 1) decode_resident(const D
     s_conv[tid] = 0;
     s_berr[tid] = 0;
   }
+  for (int i = tid; i <= g.G; i += nt) {
+    s_cn_off[i] = __ldg(g.cn_off + i);
+    s_fix_off[i] = __ldg(g.fix_off + i);
+  }
   if (a.trace)
     for (int i = tid; i < nf * a.max_iters; i += nt) a.trace[f0 * a.max_iters + i] = -1;
   __syncthreads();
   bool live = f < nf;
+  // records are prefetched one phase ahead: the first CN item of the next
+  // group and the first fix-up item of the current one
+  CnRecord<D, EXACT> next_cn;
+  if (j0 < s_cn_off[1] - s_cn_off[0]) next_cn.load(g.cn_rec + static_cast<size_t>(s_cn_off[0] + j0) * CS);
 
   const bool dump = a.max_subiters > 0;
   int sub = 0;
@@ -289,18 +302,28 @@ __global__ void __launch_bounds__(max_threads_for(D), 1) decode_resident(const D
       if (dump && sub == a.max_subiters) goto finish;
       ++sub;
       // CN phase: every (CN of the group, frame); Jacobi within the group
-      const int c0 = __ldg(g.cn_off + grp), cn = __ldg(g.cn_off + grp + 1) - c0;
-      if (live) {
+      const int c0 = s_cn_off[grp], cn = s_cn_off[grp + 1] - c0;
+      const int x0 = s_fix_off[grp], xn = s_fix_off[grp + 1] - x0;
+      int4 fix_first = make_int4(0, 0, 0, 0);
+      if (j0 < xn) fix_first = __ldg(fix_vn + static_cast<size_t>(x0 + j0) * vs4);
+      if (live && j0 < cn) {
+        cn_update<D, EXACT, FPC>(c2v, P, next_cn);
         const int32_t* rec = g.cn_rec + static_cast<size_t>(c0) * CS;
-        for (int j = j0; j < cn; j += jstep) cn_update<D, EXACT, FPC>(c2v, P, rec + j * CS);
+        for (int j = j0 + jstep; j < cn; j += jstep) cn_update<D, EXACT, FPC>(c2v, P, CnRecord<D, EXACT>(rec + j * CS));
+      }
+      {
+        const int ng = grp + 1 < g.G ? grp + 1 : 0;
+        if (j0 < s_cn_off[ng + 1] - s_cn_off[ng])
+          next_cn.load(g.cn_rec + static_cast<size_t>(s_cn_off[ng] + j0) * CS);
       }
       __syncthreads();
       // VNs shared by two or more CNs of the group: exact re-sum
-      const int x0 = __ldg(g.fix_off + grp), xn = __ldg(g.fix_off + grp + 1) - x0;
       if (xn > 0) {
-        if (live)
-          vn_sum_range<FPC, VS>(c2v, P, L, reinterpret_cast<const int4*>(g.fix_rec) + static_cast<size_t>(x0) * vs4,
-                                vs4, j0, xn, jstep);
+        if (live && j0 < xn) {
+          const int4* rec = fix_vn + static_cast<size_t>(x0) * vs4;
+          vn_sum<FPC, VS>(c2v, P, L, rec + j0 * vs4, vs4, fix_first);
+          vn_sum_range<FPC, VS>(c2v, P, L, rec, vs4, j0 + jstep, xn, jstep);
+        }
         __syncthreads();
       }
     }
@@ -489,20 +512,25 @@ Plan plan_decode(const DevGraph& g, int64_t frames) {
   Plan p;
   const size_t limit = static_cast<size_t>(device_smem_optin()) - 1024;
   const size_t per = frame_bytes(g);
-  auto bytes = [&](int f) { return f * per + 20 * f + 16; };
+  auto bytes = [&](int f) { return f * per + 20 * f + 8 * (g.G + 1) + 16; };
   int fpc = g_tune_fpc.load();
   if (fpc <= 0) {
-    // largest FPC that still lets two CTAs share an SM (their barriers and
-    // latencies overlap); else the largest that fits at all
-    const size_t sm_bytes = static_cast<size_t>(device_smem_per_sm()) - 2048;
-    fpc = 8;
-    while (fpc > 1 && (bytes(fpc) > limit || 2 * bytes(fpc) > sm_bytes)) fpc /= 2;
-    if (bytes(fpc) > limit || 2 * bytes(fpc) > sm_bytes) fpc = 1;
+    // largest FPC that still lets four CTAs share an SM (their barriers and
+    // latencies overlap; measured best on the C1 code), relaxing to two, then
+    // to whatever fits
+    const size_t sm_bytes = static_cast<size_t>(device_smem_per_sm()) - 4096;
+    fpc = 0;
+    for (int ctas : {4, 2, 1}) {
+      for (int c = 8; c >= 1 && fpc == 0; c /= 2)
+        if (bytes(c) <= limit && static_cast<size_t>(ctas) * bytes(c) <= sm_bytes) fpc = c;
+      if (fpc) break;
+    }
+    if (fpc == 0) fpc = 1;
   }
   if (bytes(fpc) > limit) return p;  // does not fit: no resident plan
   int bucket = 0;
   if (!pick_kernel(g, fpc, &bucket)) return p;
-  const int max_nt = bucket <= 6 ? 1024 : (bucket <= 16 ? 512 : 256);
+  const int max_nt = bucket <= 8 ? 512 : (bucket <= 16 ? 256 : 128);
   int nt = g_tune_threads.load();
   if (nt <= 0) {
     // one CN item per thread for the largest group, in whole warps
