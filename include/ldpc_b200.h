@@ -120,15 +120,19 @@ int ldpcb_decode_device(ldpcb_code code, ldpcb_schedule s, int64_t frames, const
                         uint8_t *d_converged, float *d_posterior, int32_t *d_syndrome_trace, int64_t *d_counters,
                         void *stream);
 /* Same from host memory (pinned for best overlap); H2D / decode / D2H are
- * chunked and overlapped on two streams; blocks until done. */
+ * chunked and overlapped on two streams; blocks until done. Runs on the
+ * calling thread's current CUDA device. */
 int ldpcb_decode_host(ldpcb_code code, ldpcb_schedule s, int64_t frames, const float *llr, int max_iters,
                       int early_stop, uint8_t *bits, int bits_packed, int32_t *iterations, uint8_t *converged,
-                      float *posterior, int64_t *counters);
+                      float *posterior, int32_t *syndrome_trace, int64_t *counters);
 /* Monte-Carlo frames [frame_begin, frame_begin+frames): device channel +
  * decode + counters (run_frame + aggregation, sim.hpp:111-124, 162-181) */
 int ldpcb_simulate_device(ldpcb_code code, ldpcb_schedule s, double sigma2, uint64_t channel_seed,
                           int64_t frame_begin, int64_t frames, int max_iters, int early_stop, int64_t *d_counters,
                           void *stream);
+/* ldpcb_simulate_device with host counters; blocks until done */
+int ldpcb_simulate_host(ldpcb_code code, ldpcb_schedule s, double sigma2, uint64_t channel_seed, int64_t frame_begin,
+                        int64_t frames, int max_iters, int early_stop, int64_t *counters);
 /* check_update (decoder.hpp:59-87) on rows x degree explicit inputs */
 int ldpcb_check_update_device(int degree, int64_t rows, const float *d_v2c, float *d_c2v, void *stream);
 /* init_state + n_subiters x run_subiteration (decoder.hpp:39-52, 112-127),

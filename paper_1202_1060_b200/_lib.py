@@ -61,8 +61,9 @@ _SIGS = {
     ),
     "ldpcb_decode_host": (
         C.c_int,
-        [vp, vp, i64, vp, C.c_int, C.c_int, vp, C.c_int, vp, vp, vp, vp],
+        [vp, vp, i64, vp, C.c_int, C.c_int, vp, C.c_int, vp, vp, vp, vp, vp],
     ),
+    "ldpcb_simulate_host": (C.c_int, [vp, vp, dbl, u64, i64, i64, C.c_int, C.c_int, vp]),
     "ldpcb_simulate_device": (C.c_int, [vp, vp, dbl, u64, i64, i64, C.c_int, C.c_int, vp, vp]),
     "ldpcb_check_update_device": (C.c_int, [C.c_int, i64, vp, vp, vp]),
     "ldpcb_run_subiterations_device": (C.c_int, [vp, vp, i64, vp, C.c_int, vp, vp, vp]),

@@ -393,6 +393,7 @@ def decode_host(
     converged=None,
     posterior=None,
     counters=None,
+    syndrome_trace=None,
 ):
     """decode() from host memory (numpy / pinned torch CPU tensors); blocks."""
     F = llr.shape[0]
@@ -409,6 +410,7 @@ def decode_host(
             _vp(iterations),
             _vp(converged),
             _vp(posterior),
+            _vp(syndrome_trace),
             _vp(counters),
         ),
         "decode_host",

@@ -465,7 +465,7 @@ int ldpcb_decode_device(ldpcb_code code, ldpcb_schedule s, int64_t frames, const
 
 int ldpcb_decode_host(ldpcb_code code, ldpcb_schedule s, int64_t frames, const float* llr, int max_iters,
                       int early_stop, uint8_t* bits, int bits_packed, int32_t* iterations, uint8_t* converged,
-                      float* posterior, int64_t* counters) {
+                      float* posterior, int32_t* trace, int64_t* counters) {
   return guard([&] {
     check_pair(code, s);
     need(max_iters >= 1, "max_iters must be >= 1");
@@ -489,6 +489,7 @@ int ldpcb_decode_host(ldpcb_code code, ldpcb_schedule s, int64_t frames, const f
       int32_t* it = nullptr;
       uint8_t* cv = nullptr;
       float* post = nullptr;
+      int32_t* trace = nullptr;
       int64_t* cnt = nullptr;
     } buf[kSlots];
     for (int k = 0; k < kSlots; ++k) {
@@ -498,6 +499,8 @@ int ldpcb_decode_host(ldpcb_code code, ldpcb_schedule s, int64_t frames, const f
       if (iterations) cuda_check(cudaMallocAsync(&buf[k].it, chunk * sizeof(int32_t), st[k]), "cudaMallocAsync");
       if (converged) cuda_check(cudaMallocAsync(&buf[k].cv, chunk, st[k]), "cudaMallocAsync");
       if (posterior) cuda_check(cudaMallocAsync(&buf[k].post, chunk * n * sizeof(float), st[k]), "cudaMallocAsync");
+      if (trace)
+        cuda_check(cudaMallocAsync(&buf[k].trace, chunk * max_iters * sizeof(int32_t), st[k]), "cudaMallocAsync");
       if (counters) {
         cuda_check(cudaMallocAsync(&buf[k].cnt, 6 * sizeof(int64_t), st[k]), "cudaMallocAsync");
         cuda_check(cudaMemsetAsync(buf[k].cnt, 0, 6 * sizeof(int64_t), st[k]), "cudaMemsetAsync");
@@ -519,8 +522,13 @@ int ldpcb_decode_host(ldpcb_code code, ldpcb_schedule s, int64_t frames, const f
       a.iterations = buf[k].it;
       a.converged = buf[k].cv;
       a.posterior = buf[k].post;
+      a.trace = buf[k].trace;
       a.counters = reinterpret_cast<unsigned long long*>(buf[k].cnt);
       launch(ldpcb::launch_decode(g, a, st[k], nullptr), "decode kernel");
+      if (trace)
+        cuda_check(cudaMemcpyAsync(trace + c0 * max_iters, buf[k].trace, cnt * max_iters * sizeof(int32_t),
+                                   cudaMemcpyDeviceToHost, st[k]),
+                   "D2H");
       if (bits) cuda_check(cudaMemcpyAsync(bits + c0 * nb, buf[k].bits, cnt * nb, cudaMemcpyDeviceToHost, st[k]), "D2H");
       if (iterations)
         cuda_check(cudaMemcpyAsync(iterations + c0, buf[k].it, cnt * sizeof(int32_t), cudaMemcpyDeviceToHost, st[k]),
@@ -544,6 +552,7 @@ int ldpcb_decode_host(ldpcb_code code, ldpcb_schedule s, int64_t frames, const f
       if (buf[k].it) cudaFreeAsync(buf[k].it, st[k]);
       if (buf[k].cv) cudaFreeAsync(buf[k].cv, st[k]);
       if (buf[k].post) cudaFreeAsync(buf[k].post, st[k]);
+      if (buf[k].trace) cudaFreeAsync(buf[k].trace, st[k]);
       if (buf[k].cnt) cudaFreeAsync(buf[k].cnt, st[k]);
       cuda_check(cudaStreamSynchronize(st[k]), "sync");
       cudaStreamDestroy(st[k]);
@@ -584,6 +593,40 @@ int ldpcb_simulate_device(ldpcb_code code, ldpcb_schedule s, double sigma2, uint
     }
     cuda_check(cudaFreeAsync(scratch, st), "cudaFreeAsync");
     return LDPCB_OK;
+  });
+}
+
+int ldpcb_simulate_host(ldpcb_code code, ldpcb_schedule s, double sigma2, uint64_t channel_seed, int64_t frame_begin,
+                        int64_t frames, int max_iters, int early_stop, int64_t* counters) {
+  return guard([&] {
+    check_pair(code, s);
+    need(counters != nullptr, "null counters");
+    cudaStream_t st;
+    cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+    int64_t* d = nullptr;
+    int rc = LDPCB_OK;
+    try {
+      cuda_check(cudaMallocAsync(&d, 6 * sizeof(int64_t), st), "cudaMallocAsync");
+      cuda_check(cudaMemsetAsync(d, 0, 6 * sizeof(int64_t), st), "cudaMemsetAsync");
+      rc = ldpcb_simulate_device(code, s, sigma2, channel_seed, frame_begin, frames, max_iters, early_stop, d, st);
+      if (rc == LDPCB_OK) {
+        int64_t h[6];
+        cuda_check(cudaMemcpyAsync(h, d, sizeof h, cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_check(cudaStreamSynchronize(st), "sync");
+        for (int i = 0; i < 6; ++i) counters[i] += h[i];
+      }
+    } catch (...) {
+      if (d) cudaFreeAsync(d, st);
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+      throw;
+    }
+    const std::string err = g_last_error;  // keep the inner message
+    cudaFreeAsync(d, st);
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    g_last_error = err;
+    return rc;
   });
 }
 

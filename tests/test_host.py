@@ -169,13 +169,13 @@ def test_decode_argument_errors_without_gpu(P):
     from paper_1202_1060_b200 import _lib
 
     with pytest.raises(ValueError, match="max_iters"):
-        _lib.check(_lib.lib.ldpcb_decode_host(g.handle, s.handle, 1, None, 0, 1, None, 0, None, None, None, None))
+        _lib.check(_lib.lib.ldpcb_decode_host(g.handle, s.handle, 1, None, 0, 1, None, 0, None, None, None, None, None))
     with pytest.raises(ValueError):
         P.sigma2_from_ebn0(1.0, 0.0)
     assert P.sigma2_from_ebn0(2.0, 0.5) == 0.63095734448019325
     other = P.TannerGraph.random_regular(60, 3, 6, 1)
     so = P.GroupSchedule.flooding(other)
     with pytest.raises(ValueError, match="different code"):
-        _lib.check(_lib.lib.ldpcb_decode_host(g.handle, so.handle, 1, None, 5, 1, None, 0, None, None, None, None))
+        _lib.check(_lib.lib.ldpcb_decode_host(g.handle, so.handle, 1, None, 5, 1, None, 0, None, None, None, None, None))
     with pytest.raises(ValueError):
         P.set_tuning(3, 0)
