@@ -142,11 +142,15 @@ int ldpcb_run_subiterations_device(ldpcb_code code, ldpcb_schedule s, int64_t fr
 
 /* ---- introspection / tuning --------------------------------------------- */
 
-/* kernel: 1 = SMEM-resident; fpc = frames per CTA */
+/* kernel: 1 = SMEM-resident (fpc = frames per CTA), 2 = HBM-streamed
+ * (fpc = frames per chunk) */
 int ldpcb_decode_plan(ldpcb_code code, ldpcb_schedule s, int64_t frames, int32_t *kernel, int32_t *fpc,
                       int32_t *threads, int32_t *smem_bytes, int32_t *degree_bucket);
 /* 0 = automatic */
 int ldpcb_set_tuning(int frames_per_cta, int threads);
+/* 0 = automatic (resident when a frame fits shared memory), 1 = resident
+ * only, 2 = HBM-streamed */
+int ldpcb_set_kernel(int kernel);
 /* 1 (default): in iterations that do not test the syndrome, skip the exact
  * re-summation of the posteriors (in-place updates carry them); the totals
  * are exact whenever hard decisions are taken. 0: every iteration. */

@@ -24,6 +24,7 @@ from .api import (  # noqa: F401
     make_nondisjoint_schedule,
     plan,
     run_subiterations,
+    set_kernel,
     set_lazy_totals,
     set_tuning,
     sigma2_from_ebn0,

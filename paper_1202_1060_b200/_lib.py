@@ -71,6 +71,7 @@ _SIGS = {
     "ldpcb_set_tuning": (C.c_int, [C.c_int, C.c_int]),
     "ldpcb_kernel_launches": (i64, []),
     "ldpcb_set_lazy_totals": (C.c_int, [C.c_int]),
+    "ldpcb_set_kernel": (C.c_int, [C.c_int]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

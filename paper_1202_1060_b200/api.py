@@ -498,6 +498,11 @@ def set_tuning(frames_per_cta: int = 0, threads: int = 0) -> None:
     check(lib.ldpcb_set_tuning(frames_per_cta, threads))
 
 
+def set_kernel(kernel: int = 0) -> None:
+    """0 automatic, 1 shared-memory resident only, 2 HBM-streamed."""
+    check(lib.ldpcb_set_kernel(kernel))
+
+
 def set_lazy_totals(on: bool) -> None:
     check(lib.ldpcb_set_lazy_totals(int(on)))
 

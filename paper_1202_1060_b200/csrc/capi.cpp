@@ -197,6 +197,8 @@ ldpcb::DevGraph dev_graph(ldpcb_code code, ldpcb_schedule s) {
   g.fix_rec = d.fix_rec;
   g.all_vn_rec = d.all_vn_rec;
   g.all_rec = d.all_rec;
+  g.h_cn_off = t.cn_off.data();
+  g.h_fix_off = t.fix_off.data();
   return g;
 }
 
@@ -457,7 +459,7 @@ int ldpcb_decode_device(ldpcb_code code, ldpcb_schedule s, int64_t frames, const
     a.counters = reinterpret_cast<unsigned long long*>(d_counters);
     ldpcb::Plan p;
     const int err = ldpcb::launch_decode(g, a, stream, &p);
-    if (p.kernel == 0) throw std::runtime_error("no resident decoder plan fits this code (n too large)");
+    if (p.kernel == 0) throw std::runtime_error("no decoder plan for this code (check degree or memory)");
     launch(err, "decode kernel");
     return LDPCB_OK;
   });
@@ -476,7 +478,7 @@ int ldpcb_decode_host(ldpcb_code code, ldpcb_schedule s, int64_t frames, const f
     const int n = g.n;
     const int64_t nb = bits_packed ? (n + 7) / 8 : n;
     const ldpcb::Plan p0 = ldpcb::plan_decode(g, frames);
-    if (p0.kernel == 0) throw std::runtime_error("no resident decoder plan fits this code (n too large)");
+    if (p0.kernel == 0) throw std::runtime_error("no decoder plan for this code (check degree or memory)");
     // chunks of ~32 MB of LLRs, a multiple of the frames per CTA
     int64_t chunk = std::max<int64_t>(p0.fpc, (int64_t{32} << 20) / (4 * n));
     chunk = std::min<int64_t>(chunk, frames);
@@ -574,7 +576,7 @@ int ldpcb_simulate_device(ldpcb_code code, ldpcb_schedule s, double sigma2, uint
     if (frames == 0) return LDPCB_OK;
     const auto g = dev_graph(code, s);
     const ldpcb::Plan p0 = ldpcb::plan_decode(g, frames);
-    if (p0.kernel == 0) throw std::runtime_error("no resident decoder plan fits this code (n too large)");
+    if (p0.kernel == 0) throw std::runtime_error("no decoder plan for this code (check degree or memory)");
     auto st = static_cast<cudaStream_t>(stream);
     int64_t chunk = std::max<int64_t>(p0.fpc, (int64_t{256} << 20) / (4 * g.n));
     chunk = std::min<int64_t>(chunk, frames);
@@ -655,7 +657,7 @@ int ldpcb_run_subiterations_device(ldpcb_code code, ldpcb_schedule s, int64_t fr
     a.v2c_out = d_v2c;
     ldpcb::Plan p;
     const int err = ldpcb::launch_decode(g, a, stream, &p);
-    if (p.kernel == 0) throw std::runtime_error("no resident decoder plan fits this code (n too large)");
+    if (p.kernel == 0) throw std::runtime_error("no decoder plan for this code (check degree or memory)");
     launch(err, "decode kernel");
     return LDPCB_OK;
   });
@@ -688,6 +690,14 @@ int ldpcb_set_tuning(int frames_per_cta, int threads) {
 }
 
 int64_t ldpcb_kernel_launches(void) { return ldpcb::kernel_launch_count(); }
+
+int ldpcb_set_kernel(int kernel) {
+  return guard([&] {
+    need(kernel >= 0 && kernel <= 2, "kernel must be 0 (auto), 1 (resident) or 2 (streamed)");
+    ldpcb::set_force_kernel(kernel);
+    return LDPCB_OK;
+  });
+}
 
 int ldpcb_set_lazy_totals(int on) {
   return guard([&] {

@@ -32,128 +32,17 @@
 #include <map>
 #include <mutex>
 
+#include "common.cuh"
 #include "kernels.cuh"
 #include "rng.cuh"
 
 namespace ldpcb {
 namespace {
 
-constexpr float kClamp = 30.0f;  // decoder.hpp:18
-constexpr float kLog2e = 1.4426950408889634f;
-constexpr float kLn2 = 0.69314718055994531f;
-// Inside the kernels messages are kept in log2 units (LLR * log2 e), so the
-// boxplus needs no scaling around ex2 / lg2; the clamp scales with them.
-constexpr float kClampB = 43.280851226668897f;  // 30 * log2(e)
+using namespace dev;
 
 std::atomic<int64_t> g_launches{0};
-std::atomic<int> g_tune_fpc{0}, g_tune_threads{0}, g_lazy_totals{1};
-
-__device__ __forceinline__ float mufu_ex2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ float mufu_lg2(float x) {
-  float y;
-  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
-__device__ __forceinline__ float clamp_llr(float x) { return fminf(fmaxf(x, -kClamp), kClamp); }
-__device__ __forceinline__ float clamp_bits(float x) { return fminf(fmaxf(x, -kClampB), kClampB); }
-
-// Exclusion boxplus over one CN, in log2 units. x[k] are the incoming v2c
-// for k < deg (EXACT: deg == D); |v2c| is clamped to 30 nats here
-// (decoder.hpp:125) and the sign travels in the IEEE sign bit.
-// store(k, c2v_k) receives every output, clamped to 30 nats (decoder.hpp:74).
-//
-// Exactly-zero inputs: ex2(-0) = 1 exactly, and every combine below is
-// symmetric under N <-> D of an operand equal to (a, a), so any output whose
-// exclusion set holds a zero ends with N == D bit-for-bit and a magnitude of
-// exactly 0 (decoder.hpp:77-83) without per-edge bookkeeping.
-template <int D, bool EXACT, class Store>
-__device__ __forceinline__ void boxplus_row(const float (&x)[D], int deg, Store&& store) {
-  float z[D];
-  unsigned sg = 0;
-#pragma unroll
-  for (int k = 0; k < D; ++k) {
-    if (EXACT || k < deg) {
-      sg ^= __float_as_uint(x[k]);
-      z[k] = mufu_ex2(-fminf(fabsf(x[k]), kClampB));
-    } else {
-      z[k] = 0.f;  // boxplus identity (N, D) = (0, 1)
-    }
-  }
-  auto emit = [&](int k, float num, float den) {
-    if (EXACT || k < deg) {
-      const float mag = fminf(fabsf(mufu_lg2(den) - mufu_lg2(num)), kClampB);
-      const unsigned sgn = (sg ^ __float_as_uint(x[k])) & 0x80000000u;
-      store(k, __uint_as_float(__float_as_uint(mag) | sgn));
-    }
-  };
-  // prefix p[k] = z0 (+) ... (+) zk for k <= D-2: (N, D) <- (N + z D, D + z N)
-  float pn[D > 1 ? D - 1 : 1], pd[D > 1 ? D - 1 : 1];
-  pn[0] = z[0];
-  pd[0] = 1.f;
-#pragma unroll
-  for (int k = 1; k < D - 1; ++k) {
-    pn[k] = fmaf(z[k], pd[k - 1], pn[k - 1]);
-    pd[k] = fmaf(z[k], pn[k - 1], pd[k - 1]);
-  }
-  emit(D - 1, pn[D - 2], pd[D - 2]);
-  float sn = z[D - 1], sd = 1.f;  // suffix s[k+1]
-  if (D >= 3) {  // first middle output, suffix = (z[D-1], 1): same rounding pattern without the * 1
-    constexpr int k = D >= 3 ? D - 2 : 1;
-    emit(k, __fadd_rn(pn[k - 1], __fmul_rn(sn, pd[k - 1])), __fadd_rn(pd[k - 1], __fmul_rn(pn[k - 1], sn)));
-    const float tn = z[k] + sn;
-    const float td = fmaf(z[k], sn, 1.f);
-    sn = tn;
-    sd = td;
-  }
-#pragma unroll
-  for (int k = D - 3; k >= 1; --k) {
-    // out_k = p[k-1] (+) s[k+1], rounded symmetrically (see above)
-    emit(k, __fadd_rn(__fmul_rn(pn[k - 1], sd), __fmul_rn(sn, pd[k - 1])),
-         __fadd_rn(__fmul_rn(pd[k - 1], sd), __fmul_rn(pn[k - 1], sn)));
-    const float tn = fmaf(z[k], sd, sn);
-    const float td = fmaf(z[k], sn, sd);
-    sn = tn;
-    sd = td;
-  }
-  emit(0, sn, sd);
-}
-
-// One CN record (host.hpp KernelTables): [slot of edge 0, single-touch
-// mask, v_0 ... v_{D-1}] (v = -1 past the degree).
-template <int D, bool EXACT>
-struct CnRecord {
-  static constexpr int kInts = (2 + D + 3) / 4 * 4;
-  int r[kInts];
-  CnRecord() = default;
-  __device__ __forceinline__ explicit CnRecord(const int32_t* __restrict__ p) { load(p); }
-  __device__ __forceinline__ void load(const int32_t* __restrict__ p) {
-    const int4* q = reinterpret_cast<const int4*>(p);
-#pragma unroll
-    for (int i = 0; i < kInts / 4; ++i) {
-      const int4 t = __ldg(q + i);
-      r[4 * i] = t.x;
-      r[4 * i + 1] = t.y;
-      r[4 * i + 2] = t.z;
-      r[4 * i + 3] = t.w;
-    }
-  }
-  __device__ __forceinline__ int slot() const { return r[0]; }
-  __device__ __forceinline__ unsigned mask() const { return static_cast<unsigned>(r[1]); }
-  __device__ __forceinline__ int var(int k) const { return r[2 + k]; }
-  __device__ __forceinline__ bool has(int k) const { return EXACT || r[2 + k] >= 0; }
-  __device__ __forceinline__ int deg() const {
-    if (EXACT) return D;
-    int d = 0;
-#pragma unroll
-    for (int k = 0; k < D; ++k) d += r[2 + k] >= 0;
-    return d;
-  }
-};
+std::atomic<int> g_tune_fpc{0}, g_tune_threads{0}, g_lazy_totals{1}, g_force_kernel{0};
 
 // Frame-interleaved shared-memory views of ONE frame: element i of a per-slot
 // or per-VN array lives at base[i * FPC].
@@ -504,11 +393,22 @@ void set_tuning(int fpc, int threads) {
 }
 
 int64_t kernel_launch_count() { return g_launches.load(); }
+void note_launches(int n) { g_launches += n; }
+void set_force_kernel(int kernel) { g_force_kernel = kernel; }
 
 void set_lazy_totals(int on) { g_lazy_totals = on; }
 int lazy_totals() { return g_lazy_totals.load(); }
 
+Plan plan_resident(const DevGraph& g, int64_t frames);
+
 Plan plan_decode(const DevGraph& g, int64_t frames) {
+  if (g_force_kernel.load() == 2) return plan_stream(g, frames);
+  Plan p = plan_resident(g, frames);
+  if (p.kernel == 0 && g_force_kernel.load() != 1) p = plan_stream(g, frames);
+  return p;
+}
+
+Plan plan_resident(const DevGraph& g, int64_t frames) {
   Plan p;
   const size_t limit = static_cast<size_t>(device_smem_optin()) - 1024;
   const size_t per = frame_bytes(g);
@@ -550,6 +450,7 @@ int launch_decode(const DevGraph& g, const DecodeArgs& a_in, void* stream, Plan*
   DecodeArgs a = a_in;
   a.lazy_totals = g_lazy_totals.load();
   const Plan p = plan_decode(g, a.frames);
+  if (p.kernel == 2) return launch_stream(g, a, stream, used);
   if (used) *used = p;
   if (p.kernel == 0) return static_cast<int>(cudaErrorInvalidConfiguration);
   if (a.frames <= 0) return 0;

@@ -24,6 +24,9 @@ struct DevGraph {
   const int32_t* fix_rec = nullptr;
   const int32_t* all_vn_rec = nullptr;  // [n] VN records
   const int32_t* all_rec = nullptr;     // [m] CN records, syndrome
+  // host copies of the per-group offsets (owned by the schedule handle)
+  const int32_t* h_cn_off = nullptr;
+  const int32_t* h_fix_off = nullptr;
 };
 
 // One decode launch (all pointers are device pointers; outputs nullable).
@@ -56,7 +59,7 @@ inline int cn_bucket(int max_cdeg, bool cregular) {
 inline int cn_record_stride(int bucket) { return (2 + bucket + 3) / 4 * 4; }
 
 struct Plan {
-  int kernel = 0;  // 1 = SMEM-resident frame-interleaved
+  int kernel = 0;  // 1 = SMEM-resident frame-interleaved, 2 = HBM-streamed
   int fpc = 0;     // frames per CTA
   int threads = 0;
   int smem = 0;    // dynamic shared memory bytes
@@ -71,6 +74,11 @@ int launch_channel(int n, double sigma2, uint64_t seed, int64_t frame0, int64_t 
 int launch_check_update(int degree, int64_t rows, const float* v2c, float* c2v, void* stream);
 
 void set_tuning(int fpc, int threads);
+void set_force_kernel(int kernel);  // 0 auto, 1 resident, 2 streamed
+void note_launches(int n);
+// HBM-streamed decoder (stream.cu): frames whose state does not fit one SM
+int launch_stream(const DevGraph& g, const DecodeArgs& a, void* stream, Plan* used);
+Plan plan_stream(const DevGraph& g, int64_t frames);
 void set_lazy_totals(int on);
 int lazy_totals();
 int64_t kernel_launch_count();

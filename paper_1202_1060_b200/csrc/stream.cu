@@ -1,0 +1,420 @@
+// stream.cu -- HBM-streamed decoder for frames whose state does not fit one
+// SM's shared memory (BASELINE configs 4 and 5: n = 64800, 1.3 MB per frame).
+//
+// A chunk of B frames (B a multiple of 4) is decoded together. Its state
+// lives in HBM frame-interleaved, element (i, frame) at i * B + frame:
+//   c2v [n_slots][B]   P [n][B]   L [n][B]   (log2 units, as in decoder.cu)
+// Each thread serves one (CN or VN record, quad of 4 consecutive frames), so
+// every state access is a 16-byte vector load and a warp reads 512
+// contiguous bytes. Per sub-iteration of group g (decoder.hpp:112-127):
+//   stream_cn<g>      CN updates of the group, in-place posterior update of
+//                     VNs touched by one CN of the group (Jacobi-safe)
+//   stream_vnsum<g>   exact re-sum of VNs shared by two or more of its CNs
+// and per syndrome test: exact totals, syndrome weights, per-frame
+// bookkeeping (decoder.hpp:162-177). Kernel boundaries are the barriers.
+// HBM roofline: ~16 B per CN-edge update (c2v read+write, posterior
+// read+write), SURVEY.md 8(d) roofline A.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace ldpcb {
+namespace {
+
+using namespace dev;
+
+struct ChunkState {
+  int64_t B = 0;     // layout stride (frames), multiple of 4
+  int nb = 0;        // frames of this chunk that are real
+  float* c2v = nullptr;
+  float* P = nullptr;
+  float* L = nullptr;
+  int* done = nullptr;    // [B]
+  int* weight = nullptr;  // [B]
+  int* iters = nullptr;   // [B]
+  int* conv = nullptr;    // [B]
+  int* berr = nullptr;    // [B]
+};
+
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ float& lane(float4& v, int i) { return reinterpret_cast<float*>(&v)[i]; }
+
+__device__ __forceinline__ bool quad_done(const ChunkState& s, int64_t q) {
+  const int4 d = *reinterpret_cast<const int4*>(s.done + 4 * q);
+  return d.x & d.y & d.z & d.w;
+}
+
+// L = P = clamp(llr) in log2 units, transposed [nb][n] -> [n][B] through a
+// 32 x 32 shared-memory tile; padding frames (>= nb) are marked done.
+__global__ void stream_init(int n, const float* __restrict__ llr, ChunkState s) {
+  __shared__ float tile[32][33];
+  const int v0 = blockIdx.x * 32, f0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int f = f0 + r, v = v0 + threadIdx.x;
+    tile[r][threadIdx.x] = (f < s.nb && v < n) ? clamp_llr(llr[static_cast<int64_t>(f) * n + v]) * kLog2e : kClampB;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int v = v0 + r, f = f0 + threadIdx.x;
+    if (v < n && f < s.B) {
+      const float x = tile[threadIdx.x][r];
+      s.L[static_cast<int64_t>(v) * s.B + f] = x;
+      s.P[static_cast<int64_t>(v) * s.B + f] = x;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.y == 0) {
+    const int f = f0 + threadIdx.x;
+    if (f < s.B) {
+      s.done[f] = f >= s.nb;
+      s.weight[f] = 0;
+      s.iters[f] = 0;
+      s.conv[f] = 0;
+      s.berr[f] = 0;
+    }
+  }
+}
+
+// CN phase of one group over (record, quad) items.
+template <int D, bool EXACT>
+__global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ recs, int count, ChunkState s) {
+  constexpr int CS = CnRecord<D, EXACT>::kInts;
+  const int64_t QB = s.B / 4;
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (item >= count * QB) return;
+  const int j = static_cast<int>(item / QB);
+  const int64_t q = item - j * QB;
+  if (quad_done(s, q)) return;
+  const CnRecord<D, EXACT> cr(recs + static_cast<int64_t>(j) * CS);
+  const int base = cr.slot();
+  const unsigned mask = cr.mask();
+  const int deg = cr.deg();
+  float4 pv[D], old[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    if (cr.has(k)) {
+      pv[k] = ld4(s.P + static_cast<int64_t>(cr.var(k)) * s.B + 4 * q);
+      old[k] = ld4(s.c2v + static_cast<int64_t>(base + k) * s.B + 4 * q);
+    } else {
+      pv[k] = old[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  float4 out[D];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float x[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) x[k] = lane(pv[k], i) - lane(old[k], i);
+    boxplus_row<D, EXACT>(x, deg, [&](int k, float c) { lane(out[k], i) = c; });
+  }
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    if (!cr.has(k)) continue;
+    st4(s.c2v + static_cast<int64_t>(base + k) * s.B + 4 * q, out[k]);
+    if (mask & (1u << k)) {
+      float4 p = pv[k];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) lane(p, i) += lane(out[k], i) - lane(old[k], i);
+      st4(s.P + static_cast<int64_t>(cr.var(k)) * s.B + 4 * q, p);
+    }
+  }
+}
+
+// P_v = L_v + sum of c2v over the VN's edges, ascending CN order (the totals
+// of decoder.hpp:162-165), over (VN record, quad) items.
+__global__ void __launch_bounds__(256) stream_vnsum(const int4* __restrict__ recs, int vs4, int count, ChunkState s,
+                                                    int skip_done) {
+  const int64_t QB = s.B / 4;
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (item >= count * QB) return;
+  const int j = static_cast<int>(item / QB);
+  const int64_t q = item - j * QB;
+  if (skip_done && quad_done(s, q)) return;
+  const int4* rec = recs + static_cast<int64_t>(j) * vs4;
+  int4 t = __ldg(rec);
+  const int v = t.x;
+  float4 acc = ld4(s.L + static_cast<int64_t>(v) * s.B + 4 * q);
+  auto add = [&](int slot) {
+    const float4 c = ld4(s.c2v + static_cast<int64_t>(slot) * s.B + 4 * q);
+    acc.x += c.x;
+    acc.y += c.y;
+    acc.z += c.z;
+    acc.w += c.w;
+  };
+  add(t.y);
+  add(t.z);
+  add(t.w);
+  for (int r = 1; r < vs4; ++r) {
+    t = __ldg(rec + r);
+    add(t.x);
+    add(t.y);
+    add(t.z);
+    add(t.w);
+  }
+  st4(s.P + static_cast<int64_t>(v) * s.B + 4 * q, acc);
+}
+
+// Syndrome weight per frame (decoder.hpp:129-137) over (CN, quad) items.
+template <int D, bool EXACT>
+__global__ void __launch_bounds__(256) stream_syndrome(const int32_t* __restrict__ recs, int m, ChunkState s) {
+  constexpr int CS = CnRecord<D, EXACT>::kInts;
+  const int64_t QB = s.B / 4;
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (item >= m * QB) return;
+  const int r = static_cast<int>(item / QB);
+  const int64_t q = item - r * QB;
+  if (quad_done(s, q)) return;
+  const CnRecord<D, EXACT> cr(recs + static_cast<int64_t>(r) * CS);
+  unsigned p = 0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    if (!cr.has(k)) continue;
+    const float4 v = ld4(s.P + static_cast<int64_t>(cr.var(k)) * s.B + 4 * q);
+    p ^= static_cast<unsigned>(v.x < 0.f) | static_cast<unsigned>(v.y < 0.f) << 1 |
+         static_cast<unsigned>(v.z < 0.f) << 2 | static_cast<unsigned>(v.w < 0.f) << 3;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (p & (1u << i)) atomicAdd(s.weight + 4 * q + i, 1);
+}
+
+// Per-frame bookkeeping after a syndrome test (decoder.hpp:170-177).
+__global__ void stream_iter_end(ChunkState s, int iter, int early_stop, int32_t* trace, int max_iters,
+                                int64_t frame0) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= s.nb || s.done[f]) return;
+  const int w = s.weight[f];
+  if (trace) trace[(frame0 + f) * max_iters + iter - 1] = w;
+  s.iters[f] = iter;
+  s.conv[f] = w == 0;
+  s.weight[f] = 0;
+  if (w == 0 && early_stop) s.done[f] = 1;
+}
+
+// Hard decisions (tie -> 0): packed or byte bits, per-frame error counts and
+// optional posteriors, transposed [n][B] -> [frames][...] through shared
+// memory. Block (32, 8): tile of 32 frames x 256 VNs.
+__global__ void stream_bits(int n, ChunkState s, uint8_t* bits, int packed, float* posterior, int64_t frame0) {
+  __shared__ unsigned char tile[32][33];
+  __shared__ float ptile[32][33];
+  const int f0 = blockIdx.y * 32, b0 = blockIdx.x * 32;  // 32 bytes = 256 VNs
+  const int nbytes = (n + 7) / 8;
+  int errs = 0;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int b = b0 + r, f = f0 + threadIdx.x;
+    unsigned byte = 0;
+    if (f < s.nb && b < nbytes)
+      for (int j = 0; j < 8; ++j) {
+        const int v = 8 * b + j;
+        if (v < n && s.P[static_cast<int64_t>(v) * s.B + f] < 0.f) byte |= 1u << j;
+      }
+    tile[threadIdx.x][r] = static_cast<unsigned char>(byte);
+    errs += __popc(byte);
+  }
+  if (errs) atomicAdd(s.berr + f0 + threadIdx.x, errs);
+  __syncthreads();
+  if (bits) {
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+      const int f = f0 + r;
+      if (f >= s.nb) continue;
+      const int b = b0 + threadIdx.x;
+      if (b >= nbytes) continue;
+      const unsigned byte = tile[r][threadIdx.x];
+      if (packed) {
+        bits[(frame0 + f) * nbytes + b] = static_cast<uint8_t>(byte);
+      } else {
+        for (int j = 0; j < 8; ++j)
+          if (8 * b + j < n) bits[(frame0 + f) * n + 8 * b + j] = static_cast<uint8_t>((byte >> j) & 1u);
+      }
+    }
+  }
+  if (posterior) {
+    for (int chunk = 0; chunk < 8; ++chunk) {  // 8 sub-tiles of 32 VNs
+      const int vb = 8 * b0 + 32 * chunk;
+      __syncthreads();
+      for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int v = vb + r, f = f0 + threadIdx.x;
+        ptile[r][threadIdx.x] = (v < n && f < s.B) ? s.P[static_cast<int64_t>(v) * s.B + f] * kLn2 : 0.f;
+      }
+      __syncthreads();
+      for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int f = f0 + r, v = vb + threadIdx.x;
+        if (f < s.nb && v < n) posterior[(frame0 + f) * n + v] = ptile[threadIdx.x][r];
+      }
+    }
+  }
+}
+
+__global__ void stream_final(ChunkState s, const DecodeArgs a, int64_t frame0) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
+  if (f < s.nb) {
+    const int it = a.early_stop ? s.iters[f] : a.max_iters;
+    if (a.iterations) a.iterations[frame0 + f] = it;
+    if (a.converged) a.converged[frame0 + f] = static_cast<uint8_t>(s.conv[f]);
+    c[0] = 1;
+    c[1] = s.berr[f];
+    c[2] = s.berr[f] > 0;
+    c[3] = s.conv[f];
+    c[4] = it;
+    c[5] = s.conv[f] ? it : 0;
+  }
+  if (!a.counters) return;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {
+    unsigned long long v = c[i];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(a.counters + i, v);
+  }
+}
+
+// c2v / v2c dumps in CN-major edge order (run_subiterations)
+__global__ void stream_dump(const DevGraph g, ChunkState s, float* c2v_out, float* v2c_out, int64_t frame0) {
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (item >= static_cast<int64_t>(g.E) * s.nb) return;
+  const int f = static_cast<int>(item % s.nb);
+  const int e = static_cast<int>(item / s.nb);
+  const float c = s.c2v[static_cast<int64_t>(__ldg(g.edge_slot + e)) * s.B + f];
+  if (c2v_out) c2v_out[(frame0 + f) * g.E + e] = c * kLn2;
+  if (v2c_out)
+    v2c_out[(frame0 + f) * g.E + e] = clamp_bits(s.P[static_cast<int64_t>(__ldg(g.cols + e)) * s.B + f] - c) * kLn2;
+}
+
+struct StreamKernels {
+  void (*cn)(const int32_t*, int, ChunkState);
+  void (*syn)(const int32_t*, int, ChunkState);
+};
+
+StreamKernels pick(const DevGraph& g) {
+  switch (cn_bucket(g.max_cdeg, g.cregular)) {
+    case 3: return {stream_cn<3, true>, stream_syndrome<3, true>};
+    case 6: return {stream_cn<6, true>, stream_syndrome<6, true>};
+    case 8: return {stream_cn<8, false>, stream_syndrome<8, false>};
+    case 16: return {stream_cn<16, false>, stream_syndrome<16, false>};
+    default: return {nullptr, nullptr};
+  }
+}
+
+size_t chunk_bytes_per_frame(const DevGraph& g) {
+  return 4ull * (static_cast<size_t>(g.n_slots) + 2ull * g.n) + 20;
+}
+
+unsigned blocks_for(int64_t items, int tpb) { return static_cast<unsigned>((items + tpb - 1) / tpb); }
+
+}  // namespace
+
+Plan plan_stream(const DevGraph& g, int64_t frames) {
+  Plan p;
+  if (!pick(g).cn) return p;
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 16ull << 30;
+  const size_t budget = std::min<size_t>(free_b / 3, 24ull << 30);
+  int64_t B = static_cast<int64_t>(budget / chunk_bytes_per_frame(g)) / 128 * 128;
+  B = std::min<int64_t>(B, 16384);
+  const int64_t need = (std::max<int64_t>(frames, 1) + 3) / 4 * 4;
+  B = std::min(B, need);
+  if (B < 4) return p;
+  p.kernel = 2;
+  p.fpc = static_cast<int>(B);  // frames per chunk
+  p.threads = 256;
+  p.smem = 0;
+  p.degree_bucket = cn_bucket(g.max_cdeg, g.cregular);
+  p.ctas = (frames + B - 1) / B;  // chunks
+  return p;
+}
+
+int launch_stream(const DevGraph& g, const DecodeArgs& a, void* stream_v, Plan* used) {
+  const Plan p = plan_stream(g, a.frames);
+  if (used) *used = p;
+  if (p.kernel == 0) return static_cast<int>(cudaErrorInvalidConfiguration);
+  if (a.frames <= 0) return 0;
+  auto st = static_cast<cudaStream_t>(stream_v);
+  const StreamKernels K = pick(g);
+  const int64_t B = p.fpc;
+  ChunkState s;
+  s.B = B;
+  const size_t state_bytes = 4ull * (static_cast<size_t>(g.n_slots) + 2ull * g.n) * B;
+  char* mem = nullptr;
+  cudaError_t err = cudaMallocAsync(reinterpret_cast<void**>(&mem), state_bytes + 5 * 4 * B + 256, st);
+  if (err != cudaSuccess) return static_cast<int>(err);
+  s.c2v = reinterpret_cast<float*>(mem);
+  s.P = s.c2v + static_cast<size_t>(g.n_slots) * B;
+  s.L = s.P + static_cast<size_t>(g.n) * B;
+  s.done = reinterpret_cast<int*>(s.L + static_cast<size_t>(g.n) * B);
+  s.weight = s.done + B;
+  s.iters = s.weight + B;
+  s.conv = s.iters + B;
+  s.berr = s.conv + B;
+  const int tpb = 256;
+  const int64_t QB = B / 4;
+  const bool dump = a.max_subiters > 0;
+  int launches = 0;
+  for (int64_t f0 = 0; f0 < a.frames && err == cudaSuccess; f0 += B) {
+    s.nb = static_cast<int>(std::min<int64_t>(B, a.frames - f0));
+    err = cudaMemsetAsync(s.c2v, 0, 4ull * g.n_slots * B, st);
+    if (err != cudaSuccess) break;
+    stream_init<<<dim3((g.n + 31) / 32, static_cast<unsigned>((B + 31) / 32)), dim3(32, 8), 0, st>>>(
+        g.n, a.llr + f0 * g.n, s);
+    ++launches;
+    if (a.trace) {
+      err = cudaMemsetAsync(a.trace + f0 * a.max_iters, 0xff, 4ull * s.nb * a.max_iters, st);
+      if (err != cudaSuccess) break;
+    }
+    int sub = 0;
+    bool stop = false;
+    for (int iter = 1; iter <= a.max_iters && !stop; ++iter) {
+      for (int grp = 0; grp < g.G; ++grp) {
+        if (dump && sub == a.max_subiters) {
+          stop = true;
+          break;
+        }
+        ++sub;
+        const int c0 = g.h_cn_off[grp], cn = g.h_cn_off[grp + 1] - c0;
+        if (cn > 0) {
+          K.cn<<<blocks_for(cn * QB, tpb), tpb, 0, st>>>(g.cn_rec + static_cast<size_t>(c0) * g.cs, cn, s);
+          ++launches;
+        }
+        const int x0 = g.h_fix_off[grp], xn = g.h_fix_off[grp + 1] - x0;
+        if (xn > 0) {
+          stream_vnsum<<<blocks_for(xn * QB, tpb), tpb, 0, st>>>(
+              reinterpret_cast<const int4*>(g.fix_rec) + static_cast<size_t>(x0) * g.vs4, g.vs4, xn, s, 1);
+          ++launches;
+        }
+      }
+      if (stop || dump) continue;
+      const bool check = a.early_stop || a.trace || iter == a.max_iters;
+      if (g.recompute && (check || !a.lazy_totals)) {
+        stream_vnsum<<<blocks_for(g.n * QB, tpb), tpb, 0, st>>>(reinterpret_cast<const int4*>(g.all_vn_rec), g.vs4,
+                                                                g.n, s, 1);
+        ++launches;
+      }
+      if (!check) continue;
+      K.syn<<<blocks_for(g.m * QB, tpb), tpb, 0, st>>>(g.all_rec, g.m, s);
+      stream_iter_end<<<blocks_for(s.nb, tpb), tpb, 0, st>>>(s, iter, a.early_stop, a.trace, a.max_iters, f0);
+      launches += 2;
+    }
+    if (dump) {
+      if (g.recompute)
+        stream_vnsum<<<blocks_for(g.n * QB, tpb), tpb, 0, st>>>(reinterpret_cast<const int4*>(g.all_vn_rec),
+                                                                g.vs4, g.n, s, 0);
+      stream_dump<<<blocks_for(static_cast<int64_t>(g.E) * s.nb, tpb), tpb, 0, st>>>(g, s, a.c2v_out, a.v2c_out,
+                                                                                      f0);
+      launches += 2;
+    } else {
+      const int nbytes = (g.n + 7) / 8;
+      stream_bits<<<dim3((nbytes + 31) / 32, static_cast<unsigned>((B + 31) / 32)), dim3(32, 8), 0, st>>>(
+          g.n, s, a.bits, a.bits_packed, a.posterior, f0);
+      stream_final<<<blocks_for(s.nb, tpb), tpb, 0, st>>>(s, a, f0);
+      launches += 2;
+    }
+    err = cudaGetLastError();
+  }
+  note_launches(launches);
+  cudaFreeAsync(mem, st);
+  return static_cast<int>(err);
+}
+
+}  // namespace ldpcb
