@@ -34,6 +34,8 @@ METRIC = "decoded info bits/s at fixed iterations"
 UNIT = "info bits/s"
 MUFU_PER_EDGE = 3  # SASS-counted: 1 MUFU.EX2 + 2 MUFU.LG2 per CN-edge update (decoder.cu)
 MUFU_PER_SM_CLK = 16
+HBM_BYTES_PER_EDGE = 16  # streamed decoder: c2v read + write, posterior read + write (fp32)
+DEFAULT_FRAMES = {"c5_n1008": 1 << 21, "c5_n64800": 8192}
 
 
 def parse():
@@ -43,7 +45,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--workload", default="c5_n1008")
-    ap.add_argument("--frames", type=int, default=1 << 21, help="frames per step per GPU")
+    ap.add_argument("--frames", type=int, default=0, help="frames per step per GPU (0: per-workload default)")
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU sample duration")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -61,6 +63,12 @@ def workload(name):
         s = P.configs.c1_schedules(g)["ndgsbp"]
         desc = "C5: (3,6)-regular n=1008 girth>=6 (seed 1), NDGSBP 8 windows x 84 CNs stride 63, Eb/N0 2.0 dB"
         return g, s, 2.0, desc
+    if name == "c5_n64800":
+        g = P.configs.c4_code()
+        s = P.configs.c4_schedules(g)["ndgsbp"]
+        desc = ("C5: irregular n=64800 VN degrees {2:.5,3:.4,8:.1} d_c=6 (seed 1), NDGSBP 45 windows x 960 CNs "
+                "stride 720, Eb/N0 1.1 dB")
+        return g, s, 1.1, desc
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -207,7 +215,7 @@ def run_b200(args):
     g, s, ebn0, desc = workload(args.workload)
     sigma2 = mean_sigma2(P, g, ebn0)
     P.set_tuning(args.fpc, args.threads)
-    B = args.frames
+    B = args.frames or DEFAULT_FRAMES[args.workload]
     n = g.n_vars
     K = n - g.n_checks
     stream = torch.cuda.current_stream()
@@ -262,24 +270,41 @@ def run_b200(args):
     value = total_frames * K / (elapsed_ms / 1e3)
     cnt = counters.cpu().tolist()
 
-    # ---- roofline of the dominant kernel (SFU / MUFU issue rate)
+    # ---- roofline of the dominant kernel
     edge_updates = s.edge_updates_per_iter * args.iters * B
-    mufu_achieved = edge_updates * MUFU_PER_EDGE / (kernel_ms / 1e3)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except (OSError, ValueError):
         pass
-    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    mufu_peak = n_sm * MUFU_PER_SM_CLK * sm_max * 1e6
     traffic = None
-    tf = os.path.join(ROOT, "profiles", "r01_dram_bytes_per_launch.json")
+    tf = os.path.join(ROOT, "profiles", "dram_bytes_per_launch.json")
     if os.path.exists(tf):
         try:
             traffic = json.load(open(tf)).get(args.workload)
         except (OSError, ValueError):
             traffic = None
+    if pl["kernel"] == 1:  # shared-memory resident: SFU (MUFU) issue rate
+        sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        achieved = edge_updates * MUFU_PER_EDGE / (kernel_ms / 1e3)
+        peak = n_sm * MUFU_PER_SM_CLK * sm_max * 1e6
+        roofline = {"bound": "sfu", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "GMUFU/s",
+                    "frac": achieved / peak, "traffic": traffic,
+                    "note": f"decode_resident: {MUFU_PER_EDGE} MUFU per CN-edge update x {s.edge_updates_per_iter} "
+                            f"edge updates/iter x {args.iters} iters x {B} frames per launch / CUDA-event launch "
+                            f"time {kernel_ms:.3f} ms; peak = {n_sm} SMs x {MUFU_PER_SM_CLK}/clk x {sm_max:.0f} MHz "
+                            "(MEASURED_PEAKS sm_max_mhz)"}
+    else:  # HBM-streamed: bytes
+        per_frame = args.iters * HBM_BYTES_PER_EDGE * s.edge_updates_per_iter + 4 * n + (n + 7) // 8
+        achieved = per_frame * B / (kernel_ms / 1e3)
+        peak = float(peaks.get("hbm_gbs", 6650.0)) * 1e9
+        roofline = {"bound": "hbm", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": traffic,
+                    "note": f"HBM-streamed decode ({pl['fpc']}-frame chunks, all its kernels): algorithmic "
+                            f"{per_frame / 1e6:.2f} MB/frame = {args.iters} iters x {HBM_BYTES_PER_EDGE} B x "
+                            f"{s.edge_updates_per_iter} CN-edge updates + LLR in + bits out, x {B} frames / "
+                            f"CUDA-event time {kernel_ms:.3f} ms; peak = MEASURED_PEAKS hbm_gbs"}
 
     # ---- end to end through the host C-ABI call (pinned host buffers)
     e2e = None
@@ -340,18 +365,7 @@ def run_b200(args):
             },
             "frames_per_s": total_frames / (elapsed_ms / 1e3),
             "edge_updates_per_s": edge_updates * args.steps * world / (elapsed_ms / 1e3),
-            "roofline": {
-                "bound": "sfu",
-                "achieved": mufu_achieved / 1e9,
-                "peak": mufu_peak / 1e9,
-                "unit": "GMUFU/s",
-                "frac": mufu_achieved / mufu_peak,
-                "traffic": traffic,
-                "note": f"decode kernel: {MUFU_PER_EDGE} MUFU per CN-edge update x {s.edge_updates_per_iter} "
-                        f"edge updates/iter x {args.iters} iters x {B} frames per launch / CUDA-event launch time "
-                        f"{kernel_ms:.3f} ms; peak = {n_sm} SMs x {MUFU_PER_SM_CLK}/clk x {sm_max:.0f} MHz "
-                        "(MEASURED_PEAKS sm_max_mhz)",
-            },
+            "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

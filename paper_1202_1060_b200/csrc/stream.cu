@@ -87,7 +87,8 @@ __global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ rec
   if (item >= count * QB) return;
   const int j = static_cast<int>(item / QB);
   const int64_t q = item - j * QB;
-  if (quad_done(s, q)) return;
+  const int4 dn = *reinterpret_cast<const int4*>(s.done + 4 * q);
+  if (dn.x & dn.y & dn.z & dn.w) return;
   const CnRecord<D, EXACT> cr(recs + static_cast<int64_t>(j) * CS);
   const int base = cr.slot();
   const unsigned mask = cr.mask();
@@ -110,6 +111,13 @@ __global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ rec
     for (int k = 0; k < D; ++k) x[k] = lane(pv[k], i) - lane(old[k], i);
     boxplus_row<D, EXACT>(x, deg, [&](int k, float c) { lane(out[k], i) = c; });
   }
+  // frames that already stopped (decoder.hpp:173-177) keep their state
+  const int dl[4] = {dn.x, dn.y, dn.z, dn.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (dl[i])
+#pragma unroll
+      for (int k = 0; k < D; ++k) lane(out[k], i) = lane(old[k], i);
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     if (!cr.has(k)) continue;
