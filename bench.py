@@ -301,7 +301,7 @@ def run_b200(args):
         peak = float(peaks.get("hbm_gbs", 6650.0)) * 1e9
         roofline = {"bound": "hbm", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": traffic,
-                    "note": f"HBM-streamed decode ({pl['fpc']}-frame chunks, all its kernels): algorithmic "
+                    "note": f"HBM-streamed decode ({pl['frames_per_cta']}-frame chunks, all its kernels): algorithmic "
                             f"{per_frame / 1e6:.2f} MB/frame = {args.iters} iters x {HBM_BYTES_PER_EDGE} B x "
                             f"{s.edge_updates_per_iter} CN-edge updates + LLR in + bits out, x {B} frames / "
                             f"CUDA-event time {kernel_ms:.3f} ms; peak = MEASURED_PEAKS hbm_gbs"}
