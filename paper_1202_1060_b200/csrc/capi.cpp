@@ -169,6 +169,7 @@ void check_pair(ldpcb_code code, ldpcb_schedule s) {
 
 ldpcb::DevGraph dev_graph(ldpcb_code code, ldpcb_schedule s) {
   check_pair(code, s);
+  retain_pool_memory();
   const auto& c = code->impl->device();
   const auto& d = s->impl->device();
   const auto& h = code->impl->host;
@@ -214,6 +215,24 @@ ldpcb::Rows rows_from_csr(int m, const int32_t* off, const int32_t* cols) {
 }
 
 void launch(int err, const char* what) { cuda_check(err, what); }
+
+// Keep freed stream-ordered allocations in the device's default pool instead
+// of returning them to the driver at every synchronisation: the host entry
+// points allocate multi-GB chunk state per call.
+void retain_pool_memory() {
+  static std::mutex mu;
+  static std::map<int, bool> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[dev] = true;
+}
 
 }  // namespace
 
@@ -479,8 +498,10 @@ int ldpcb_decode_host(ldpcb_code code, ldpcb_schedule s, int64_t frames, const f
     const int64_t nb = bits_packed ? (n + 7) / 8 : n;
     const ldpcb::Plan p0 = ldpcb::plan_decode(g, frames);
     if (p0.kernel == 0) throw std::runtime_error("no decoder plan for this code (check degree or memory)");
-    // chunks of ~32 MB of LLRs, a multiple of the frames per CTA
-    int64_t chunk = std::max<int64_t>(p0.fpc, (int64_t{32} << 20) / (4 * n));
+    // chunks of ~32 MB of LLRs, a multiple of the frames per CTA; for the
+    // streamed kernel two half-size decode chunks so copies overlap decoding
+    int64_t chunk = p0.kernel == 2 ? std::max<int64_t>(4, (p0.fpc / 2 + 3) / 4 * 4)
+                                   : std::max<int64_t>(p0.fpc, (int64_t{32} << 20) / (4 * n));
     chunk = std::min<int64_t>(chunk, frames);
     chunk = (chunk + p0.fpc - 1) / p0.fpc * p0.fpc;
     const int kSlots = 2;
