@@ -162,6 +162,24 @@ int make_sched(const std::shared_ptr<CodeImpl>& code, ldpcb::ScheduleData s, ldp
   return LDPCB_OK;
 }
 
+// Keep freed stream-ordered allocations in the device's default pool instead
+// of returning them to the driver at every synchronisation: the host entry
+// points allocate multi-GB chunk state per call.
+void retain_pool_memory() {
+  static std::mutex mu;
+  static std::map<int, bool> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[dev] = true;
+}
+
 void check_pair(ldpcb_code code, ldpcb_schedule s) {
   need(code && s, "null handle");
   need(s->impl->code.get() == code->impl.get(), "schedule was built for a different code");
@@ -216,23 +234,7 @@ ldpcb::Rows rows_from_csr(int m, const int32_t* off, const int32_t* cols) {
 
 void launch(int err, const char* what) { cuda_check(err, what); }
 
-// Keep freed stream-ordered allocations in the device's default pool instead
-// of returning them to the driver at every synchronisation: the host entry
-// points allocate multi-GB chunk state per call.
-void retain_pool_memory() {
-  static std::mutex mu;
-  static std::map<int, bool> done;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return;
-  std::lock_guard<std::mutex> lk(mu);
-  if (done[dev]) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t keep = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-  }
-  done[dev] = true;
-}
+
 
 }  // namespace
 
