@@ -142,12 +142,14 @@ int ldpcb_run_subiterations_device(ldpcb_code code, ldpcb_schedule s, int64_t fr
 
 /* ---- introspection / tuning --------------------------------------------- */
 
-/* kernel: 1 = SMEM-resident (fpc = frames per CTA), 2 = HBM-streamed
- * (fpc = frames per chunk) */
+/* kernel: 2 = HBM-streamed (fpc = frames per chunk); SMEM-resident plans
+ * report 10 + frames_per_thread (11, 12) with fpc = frames per CTA */
 int ldpcb_decode_plan(ldpcb_code code, ldpcb_schedule s, int64_t frames, int32_t *kernel, int32_t *fpc,
                       int32_t *threads, int32_t *smem_bytes, int32_t *degree_bucket);
 /* 0 = automatic */
 int ldpcb_set_tuning(int frames_per_cta, int threads);
+/* frames per thread of the resident kernel: 0 = automatic, 1 or 2 */
+int ldpcb_set_frames_per_thread(int fv);
 /* 0 = automatic (resident when a frame fits shared memory), 1 = resident
  * only, 2 = HBM-streamed */
 int ldpcb_set_kernel(int kernel);

@@ -10,7 +10,7 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libldpc_b200.so")
+LIB_PATH = os.environ.get("LDPCB_LIBRARY") or os.path.join(_HERE, "libldpc_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "ldpc_b200.h")
 
 if not os.path.exists(LIB_PATH):
@@ -72,6 +72,7 @@ _SIGS = {
     "ldpcb_kernel_launches": (i64, []),
     "ldpcb_set_lazy_totals": (C.c_int, [C.c_int]),
     "ldpcb_set_kernel": (C.c_int, [C.c_int]),
+    "ldpcb_set_frames_per_thread": (C.c_int, [C.c_int]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

@@ -494,8 +494,10 @@ def plan(g: TannerGraph, s: GroupSchedule, frames: int) -> dict:
     return dict(zip(("kernel", "frames_per_cta", "threads", "smem_bytes", "degree_bucket"), (v.value for v in vals)))
 
 
-def set_tuning(frames_per_cta: int = 0, threads: int = 0) -> None:
+def set_tuning(frames_per_cta: int = 0, threads: int = 0, frames_per_thread: int = 0) -> None:
+    """Resident-kernel launch shape; 0 = automatic."""
     check(lib.ldpcb_set_tuning(frames_per_cta, threads))
+    check(lib.ldpcb_set_frames_per_thread(frames_per_thread))
 
 
 def set_kernel(kernel: int = 0) -> None:

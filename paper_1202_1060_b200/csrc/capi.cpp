@@ -691,7 +691,7 @@ int ldpcb_decode_plan(ldpcb_code code, ldpcb_schedule s, int64_t frames, int32_t
   return guard([&] {
     const auto g = dev_graph(code, s);
     const auto p = ldpcb::plan_decode(g, frames);
-    if (kernel) *kernel = p.kernel;
+    if (kernel) *kernel = p.kernel == 1 ? 10 + p.fv : p.kernel;
     if (fpc) *fpc = p.fpc;
     if (threads) *threads = p.threads;
     if (smem_bytes) *smem_bytes = p.smem;
@@ -713,6 +713,14 @@ int ldpcb_set_tuning(int frames_per_cta, int threads) {
 }
 
 int64_t ldpcb_kernel_launches(void) { return ldpcb::kernel_launch_count(); }
+
+int ldpcb_set_frames_per_thread(int fv) {
+  return guard([&] {
+    need(fv >= 0 && fv <= 2, "frames per thread must be 0 (auto), 1 or 2");
+    ldpcb::set_frames_per_thread(fv);
+    return LDPCB_OK;
+  });
+}
 
 int ldpcb_set_kernel(int kernel) {
   return guard([&] {

@@ -42,10 +42,12 @@ namespace {
 using namespace dev;
 
 std::atomic<int64_t> g_launches{0};
-std::atomic<int> g_tune_fpc{0}, g_tune_threads{0}, g_lazy_totals{1}, g_force_kernel{0};
+std::atomic<int> g_tune_fpc{0}, g_tune_threads{0}, g_tune_fv{0}, g_lazy_totals{1}, g_force_kernel{0};
 
-// Frame-interleaved shared-memory views of ONE frame: element i of a per-slot
-// or per-VN array lives at base[i * FPC].
+// Frame-interleaved shared memory: element i of a per-slot or per-VN array of
+// frame f lives at [i * FPC + f]. A thread serves FV adjacent frames (one
+// 32-bit or 64-bit shared access per element), so graph records, index math
+// and loop overhead are shared by FV frames and FV boxplus chains interleave.
 //   c2v : [n_slots] check-to-variable messages (last slot stays zero)
 //   P   : [n]       posterior = channel + all c2v (unclamped)
 //   L   : [n]       clamped channel LLR
@@ -54,95 +56,152 @@ std::atomic<int> g_tune_fpc{0}, g_tune_threads{0}, g_lazy_totals{1}, g_force_ker
 // (mask bit) gets its posterior updated in place, P += c2v_new - c2v_old:
 // no other CN of the group reads it, so the Jacobi order of
 // decoder.hpp:107-113 is kept.
-template <int D, bool EXACT, int FPC>
+template <int FV>
+struct FVec {
+  float v[FV];
+};
+
+template <int FV>
+__device__ __forceinline__ FVec<FV> lds(const float* p) {
+  FVec<FV> r;
+  if constexpr (FV == 2) {
+    const float2 t = *reinterpret_cast<const float2*>(p);
+    r.v[0] = t.x;
+    r.v[1] = t.y;
+  } else {
+#pragma unroll
+    for (int i = 0; i < FV; ++i) r.v[i] = p[i];
+  }
+  return r;
+}
+
+template <int FV>
+__device__ __forceinline__ void sts(float* p, const FVec<FV>& x) {
+  if constexpr (FV == 2) {
+    *reinterpret_cast<float2*>(p) = make_float2(x.v[0], x.v[1]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < FV; ++i) p[i] = x.v[i];
+  }
+}
+
+// live: bit i set when frame i of this thread's vector is still decoding
+template <int D, bool EXACT, int FPC, int FV>
 __device__ __forceinline__ void cn_update(float* __restrict__ c2v, float* __restrict__ P,
-                                          const CnRecord<D, EXACT>& cr) {
+                                          const CnRecord<D, EXACT>& cr, unsigned live) {
   const int base = cr.slot();
   const unsigned mask = cr.mask();
-  float x[D], pv[D], old[D];
+  const int deg = cr.deg();
+  FVec<FV> pv[D], old[D], out[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) {
-    x[k] = pv[k] = old[k] = 0.f;
     if (cr.has(k)) {
-      pv[k] = P[cr.var(k) * FPC];
-      old[k] = c2v[(base + k) * FPC];
-      x[k] = pv[k] - old[k];
+      pv[k] = lds<FV>(P + cr.var(k) * FPC);
+      old[k] = lds<FV>(c2v + (base + k) * FPC);
+    } else {
+#pragma unroll
+      for (int i = 0; i < FV; ++i) pv[k].v[i] = old[k].v[i] = 0.f;
     }
   }
-  boxplus_row<D, EXACT>(x, cr.deg(), [&](int k, float c) {
-    c2v[(base + k) * FPC] = c;
-    if (mask & (1u << k)) P[cr.var(k) * FPC] = pv[k] + (c - old[k]);
-  });
+#pragma unroll
+  for (int i = 0; i < FV; ++i) {
+    float x[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) x[k] = pv[k].v[i] - old[k].v[i];
+    boxplus_row<D, EXACT>(x, deg, [&](int k, float c) { out[k].v[i] = live & (1u << i) ? c : old[k].v[i]; });
+  }
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    if (!cr.has(k)) continue;
+    sts<FV>(c2v + (base + k) * FPC, out[k]);
+    if (mask & (1u << k)) {
+      FVec<FV> p;
+#pragma unroll
+      for (int i = 0; i < FV; ++i) p.v[i] = pv[k].v[i] + (out[k].v[i] - old[k].v[i]);
+      sts<FV>(P + cr.var(k) * FPC, p);
+    }
+  }
 }
 
 // P_v = L_v + sum of c2v over the VN's edges in ascending-CN order: the
 // totals of decoder.hpp:162-165 (and every v2c of v refreshed at once).
-template <int FPC, int VS>
+template <int FPC, int FV, int VS>
 __device__ __forceinline__ void vn_sum(const float* __restrict__ c2v, float* __restrict__ P,
-                                       const float* __restrict__ L, const int4* __restrict__ rec, int vs4,
-                                       int4 t) {
+                                       const float* __restrict__ L, const int4* __restrict__ rec, int vs4, int4 t) {
   const int v = t.x;
-  float acc = L[v * FPC] + c2v[t.y * FPC];
-  acc += c2v[t.z * FPC];
-  acc += c2v[t.w * FPC];
+  FVec<FV> acc = lds<FV>(L + v * FPC);
+  auto add = [&](int slot) {
+    const FVec<FV> c = lds<FV>(c2v + slot * FPC);
+#pragma unroll
+    for (int i = 0; i < FV; ++i) acc.v[i] += c.v[i];
+  };
+  add(t.y);
+  add(t.z);
+  add(t.w);
   const int nq = VS > 0 ? VS : vs4;
 #pragma unroll
   for (int q = 1; q < nq; ++q) {
     t = __ldg(rec + q);
-    acc += c2v[t.x * FPC];
-    acc += c2v[t.y * FPC];
-    acc += c2v[t.z * FPC];
-    acc += c2v[t.w * FPC];
+    add(t.x);
+    add(t.y);
+    add(t.z);
+    add(t.w);
   }
-  P[v * FPC] = acc;
+  sts<FV>(P + v * FPC, acc);
 }
 
 // Two independent VN records per step so their loads overlap.
-template <int FPC, int VS>
+template <int FPC, int FV, int VS>
 __device__ __forceinline__ void vn_sum_range(const float* __restrict__ c2v, float* __restrict__ P,
                                              const float* __restrict__ L, const int4* __restrict__ rec, int vs4,
                                              int j0, int count, int jstep) {
   int j = j0;
   for (; j + jstep < count; j += 2 * jstep) {
     const int4 a = __ldg(rec + j * vs4), b = __ldg(rec + (j + jstep) * vs4);
-    vn_sum<FPC, VS>(c2v, P, L, rec + j * vs4, vs4, a);
-    vn_sum<FPC, VS>(c2v, P, L, rec + (j + jstep) * vs4, vs4, b);
+    vn_sum<FPC, FV, VS>(c2v, P, L, rec + j * vs4, vs4, a);
+    vn_sum<FPC, FV, VS>(c2v, P, L, rec + (j + jstep) * vs4, vs4, b);
   }
-  if (j < count) vn_sum<FPC, VS>(c2v, P, L, rec + j * vs4, vs4, __ldg(rec + j * vs4));
+  if (j < count) vn_sum<FPC, FV, VS>(c2v, P, L, rec + j * vs4, vs4, __ldg(rec + j * vs4));
 }
 
-template <int D, bool EXACT, int FPC>
-__device__ __forceinline__ int parity(const float* __restrict__ P, const int32_t* __restrict__ rec) {
+// parity bit of each frame of the vector
+template <int D, bool EXACT, int FPC, int FV>
+__device__ __forceinline__ unsigned parity(const float* __restrict__ P, const int32_t* __restrict__ rec) {
   const CnRecord<D, EXACT> cr(rec);
   unsigned p = 0;
 #pragma unroll
   for (int k = 0; k < D; ++k)
-    if (cr.has(k)) p ^= static_cast<unsigned>(P[cr.var(k) * FPC] < 0.f);
-  return static_cast<int>(p);
+    if (cr.has(k)) {
+      const FVec<FV> x = lds<FV>(P + cr.var(k) * FPC);
+#pragma unroll
+      for (int i = 0; i < FV; ++i) p ^= static_cast<unsigned>(x.v[i] < 0.f) << i;
+    }
+  return p;
 }
 
-constexpr int max_threads_for(int D) { return D <= 8 ? 512 : (D <= 16 ? 256 : 128); }
+constexpr int max_threads_for(int D, int FV) { return FV == 2 ? 256 : (D <= 8 ? 512 : (D <= 16 ? 256 : 128)); }
 
-// Each thread serves one frame (f = tid % FPC, blockDim a multiple of 32 and
-// FPC | 32) and walks the items of that frame with stride blockDim / FPC.
-template <int D, bool EXACT, int FPC, int VS>
-__global__ void __launch_bounds__(max_threads_for(D), D <= 8 ? 2 : 1) decode_resident(const DevGraph g, const DecodeArgs a) {
+template <int D, bool EXACT, int FPC, int FV, int VS>
+__global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode_resident(const DevGraph g,
+                                                                                          const DecodeArgs a) {
   constexpr int CS = CnRecord<D, EXACT>::kInts;
+  constexpr int NG = FPC / FV;  // frame vectors per CTA
   extern __shared__ __align__(16) float smem[];
   __shared__ int s_active;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int n = g.n, m = g.m, S = g.n_slots;
   const int vs4 = VS > 0 ? VS : g.vs4;
-  const int f = tid % FPC, j0 = tid / FPC, jstep = nt / FPC;
-  float* const c2v = smem + f;
-  float* const P = smem + S * FPC + f;
+  const int fg = tid % NG, j0 = tid / NG, jstep = nt / NG;
+  const int fb = fg * FV;  // first frame of this thread's vector
+  float* const c2v = smem + fb;
+  float* const P = smem + S * FPC + fb;
   float* const L = P + n * FPC;
   int* const s_done = reinterpret_cast<int*>(smem + (S + 2 * n) * FPC);
   int* const s_weight = s_done + FPC;
   int* const s_iters = s_weight + FPC;
   int* const s_conv = s_iters + FPC;
   int* const s_berr = s_conv + FPC;
-  int* const s_cn_off = s_berr + FPC;       // [G+1] staged group tables
+  int* const s_cn_off = s_berr + FPC;         // [G+1] staged group tables
   int* const s_fix_off = s_cn_off + g.G + 1;  // [G+1]
   const int4* const all_vn = reinterpret_cast<const int4*>(g.all_vn_rec);
   const int4* const fix_vn = reinterpret_cast<const int4*>(g.fix_rec);
@@ -150,7 +209,7 @@ __global__ void __launch_bounds__(max_threads_for(D), D <= 8 ? 2 : 1) decode_res
   const int64_t f0 = static_cast<int64_t>(blockIdx.x) * FPC;
   const int nf = static_cast<int>(min(static_cast<int64_t>(FPC), a.frames - f0));
 
-  // ---- prologue: init_state (decoder.hpp:39-52) in posterior form
+  // ---- prologue: init_state (decoder.hpp:39-52) in posterior form, log2 units
   {
     const float* llr = a.llr + f0 * n;
     for (int i = tid; i < nf * n; i += nt) {
@@ -158,6 +217,11 @@ __global__ void __launch_bounds__(max_threads_for(D), D <= 8 ? 2 : 1) decode_res
       const float x = clamp_llr(__ldg(llr + i)) * kLog2e;
       smem[(S + v) * FPC + ff] = x;
       smem[(S + n + v) * FPC + ff] = x;
+    }
+    for (int i = nf * n + tid; i < FPC * n; i += nt) {  // padding frames: saturated zero codeword
+      const int ff = i / n, v = i - ff * n;
+      smem[(S + v) * FPC + ff] = kClampB;
+      smem[(S + n + v) * FPC + ff] = kClampB;
     }
     const int total = S * FPC;
     float4* c4 = reinterpret_cast<float4*>(smem);
@@ -178,7 +242,13 @@ __global__ void __launch_bounds__(max_threads_for(D), D <= 8 ? 2 : 1) decode_res
   if (a.trace)
     for (int i = tid; i < nf * a.max_iters; i += nt) a.trace[f0 * a.max_iters + i] = -1;
   __syncthreads();
-  bool live = f < nf;
+  auto live_bits = [&](int first) {
+    unsigned b = 0;
+#pragma unroll
+    for (int i = 0; i < FV; ++i) b |= static_cast<unsigned>(!s_done[first + i]) << i;
+    return b;
+  };
+  unsigned live = live_bits(fb);
   // records are prefetched one phase ahead: the first CN item of the next
   // group and the first fix-up item of the current one
   CnRecord<D, EXACT> next_cn;
@@ -190,15 +260,16 @@ __global__ void __launch_bounds__(max_threads_for(D), D <= 8 ? 2 : 1) decode_res
     for (int grp = 0; grp < g.G; ++grp) {
       if (dump && sub == a.max_subiters) goto finish;
       ++sub;
-      // CN phase: every (CN of the group, frame); Jacobi within the group
+      // CN phase: every (CN of the group, frame vector); Jacobi within the group
       const int c0 = s_cn_off[grp], cn = s_cn_off[grp + 1] - c0;
       const int x0 = s_fix_off[grp], xn = s_fix_off[grp + 1] - x0;
       int4 fix_first = make_int4(0, 0, 0, 0);
       if (j0 < xn) fix_first = __ldg(fix_vn + static_cast<size_t>(x0 + j0) * vs4);
       if (live && j0 < cn) {
-        cn_update<D, EXACT, FPC>(c2v, P, next_cn);
         const int32_t* rec = g.cn_rec + static_cast<size_t>(c0) * CS;
-        for (int j = j0 + jstep; j < cn; j += jstep) cn_update<D, EXACT, FPC>(c2v, P, CnRecord<D, EXACT>(rec + j * CS));
+        cn_update<D, EXACT, FPC, FV>(c2v, P, next_cn, live);
+        for (int j = j0 + jstep; j < cn; j += jstep)
+          cn_update<D, EXACT, FPC, FV>(c2v, P, CnRecord<D, EXACT>(rec + j * CS), live);
       }
       {
         const int ng = grp + 1 < g.G ? grp + 1 : 0;
@@ -206,30 +277,37 @@ __global__ void __launch_bounds__(max_threads_for(D), D <= 8 ? 2 : 1) decode_res
           next_cn.load(g.cn_rec + static_cast<size_t>(s_cn_off[ng] + j0) * CS);
       }
       __syncthreads();
-      // VNs shared by two or more CNs of the group: exact re-sum
+      // VNs shared by two or more CNs of the group: exact re-sum (a stopped
+      // frame re-sums to the value it already holds)
       if (xn > 0) {
         if (live && j0 < xn) {
           const int4* rec = fix_vn + static_cast<size_t>(x0) * vs4;
-          vn_sum<FPC, VS>(c2v, P, L, rec + j0 * vs4, vs4, fix_first);
-          vn_sum_range<FPC, VS>(c2v, P, L, rec, vs4, j0 + jstep, xn, jstep);
+          vn_sum<FPC, FV, VS>(c2v, P, L, rec + j0 * vs4, vs4, fix_first);
+          vn_sum_range<FPC, FV, VS>(c2v, P, L, rec, vs4, j0 + jstep, xn, jstep);
         }
         __syncthreads();
       }
     }
     if (dump) continue;
-    // ---- exact totals once per iteration (decoder.hpp:162-165); this also
-    // removes the rounding of the in-place posterior updates
     const bool check = a.early_stop || a.trace || iter == a.max_iters;
+    // ---- exact totals (decoder.hpp:162-165): removes the rounding of the
+    // in-place posterior updates before hard decisions are taken
     if (g.recompute && (check || !a.lazy_totals)) {
-      if (live) vn_sum_range<FPC, VS>(c2v, P, L, all_vn, vs4, j0, n, jstep);
+      if (live) vn_sum_range<FPC, FV, VS>(c2v, P, L, all_vn, vs4, j0, n, jstep);
       __syncthreads();
     }
     if (!check) continue;
     // ---- hard decision + syndrome weight (decoder.hpp:166-171)
     if (live) {
-      int w = 0;
-      for (int j = j0; j < m; j += jstep) w += parity<D, EXACT, FPC>(P, g.all_rec + j * CS);
-      if (w) atomicAdd(&s_weight[f], w);
+      int w[FV] = {};
+      for (int j = j0; j < m; j += jstep) {
+        const unsigned p = parity<D, EXACT, FPC, FV>(P, g.all_rec + j * CS);
+#pragma unroll
+        for (int i = 0; i < FV; ++i) w[i] += (p >> i) & 1u;
+      }
+#pragma unroll
+      for (int i = 0; i < FV; ++i)
+        if (w[i]) atomicAdd(&s_weight[fb + i], w[i]);
     }
     __syncthreads();
     if (tid == 0) {
@@ -249,26 +327,31 @@ __global__ void __launch_bounds__(max_threads_for(D), D <= 8 ? 2 : 1) decode_res
       s_active = active;
     }
     __syncthreads();
-    live = !s_done[f];
+    live = live_bits(fb);
     if (s_active == 0) break;
   }
 finish:
   __syncthreads();
   if (dump) {
-    if (g.recompute && f < nf) vn_sum_range<FPC, VS>(c2v, P, L, all_vn, vs4, j0, n, jstep);
+    if (g.recompute) vn_sum_range<FPC, FV, VS>(c2v, P, L, all_vn, vs4, j0, n, jstep);
     __syncthreads();
-    if (f < nf) {
-      const int E = g.E;
+    const int E = g.E;
+#pragma unroll
+    for (int i = 0; i < FV; ++i) {
+      if (fb + i >= nf) continue;
       for (int e = j0; e < E; e += jstep) {
-        const float c = c2v[__ldg(g.edge_slot + e) * FPC];
-        if (a.c2v_out) a.c2v_out[(f0 + f) * E + e] = c * kLn2;
-        if (a.v2c_out) a.v2c_out[(f0 + f) * E + e] = clamp_bits(P[__ldg(g.cols + e) * FPC] - c) * kLn2;
+        const float c = c2v[__ldg(g.edge_slot + e) * FPC + i];
+        if (a.c2v_out) a.c2v_out[(f0 + fb + i) * E + e] = c * kLn2;
+        if (a.v2c_out) a.v2c_out[(f0 + fb + i) * E + e] = clamp_bits(P[__ldg(g.cols + e) * FPC + i] - c) * kLn2;
       }
     }
     return;
   }
   // ---- epilogue: hard decisions (tie -> 0, decoder.hpp:166), error counts
-  if (f < nf) {
+#pragma unroll
+  for (int i = 0; i < FV; ++i) {
+    const int f = fb + i;
+    if (f >= nf) continue;
     int errs = 0;
     if (a.bits && a.bits_packed) {
       const int nb = (n + 7) >> 3;
@@ -278,21 +361,21 @@ finish:
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int v = b * 8 + j;
-          if (v < n && P[v * FPC] < 0.f) byte |= 1u << j;
+          if (v < n && P[v * FPC + i] < 0.f) byte |= 1u << j;
         }
         out[b] = static_cast<uint8_t>(byte);
         errs += __popc(byte);
       }
     } else if (a.bits || a.counters) {
       for (int v = j0; v < n; v += jstep) {
-        const int bit = P[v * FPC] < 0.f;
+        const int bit = P[v * FPC + i] < 0.f;
         if (a.bits) a.bits[(f0 + f) * n + v] = static_cast<uint8_t>(bit);
         errs += bit;
       }
     }
     if (errs) atomicAdd(&s_berr[f], errs);
     if (a.posterior)
-      for (int v = j0; v < n; v += jstep) a.posterior[(f0 + f) * n + v] = P[v * FPC] * kLn2;
+      for (int v = j0; v < n; v += jstep) a.posterior[(f0 + f) * n + v] = P[v * FPC + i] * kLn2;
   }
   if (tid < nf) {
     const int it = a.early_stop ? s_iters[tid] : a.max_iters;
@@ -339,25 +422,34 @@ __global__ void check_update_kernel(int deg, int64_t rows, const float* __restri
 using KernelFn = void (*)(const DevGraph, const DecodeArgs);
 
 template <int D, bool EXACT, int VS>
-KernelFn pick_fpc(int fpc) {
+KernelFn pick_fpc(int fpc, int fv) {
+  if (fv == 2 && D <= 8) {
+    switch (fpc) {
+      case 2: return decode_resident<D, EXACT, 2, 2, VS>;
+      case 4: return decode_resident<D, EXACT, 4, 2, VS>;
+      case 8: return decode_resident<D, EXACT, 8, 2, VS>;
+      default: return nullptr;
+    }
+  }
+  if (fv != 1) return nullptr;
   switch (fpc) {
-    case 1: return decode_resident<D, EXACT, 1, VS>;
-    case 2: return decode_resident<D, EXACT, 2, VS>;
-    case 4: return decode_resident<D, EXACT, 4, VS>;
-    case 8: return decode_resident<D, EXACT, 8, VS>;
-    case 16: return decode_resident<D, EXACT, 16, VS>;
+    case 1: return decode_resident<D, EXACT, 1, 1, VS>;
+    case 2: return decode_resident<D, EXACT, 2, 1, VS>;
+    case 4: return decode_resident<D, EXACT, 4, 1, VS>;
+    case 8: return decode_resident<D, EXACT, 8, 1, VS>;
+    case 16: return decode_resident<D, EXACT, 16, 1, VS>;
     default: return nullptr;
   }
 }
 
-KernelFn pick_kernel(const DevGraph& g, int fpc, int* bucket) {
+KernelFn pick_kernel(const DevGraph& g, int fpc, int fv, int* bucket) {
   *bucket = cn_bucket(g.max_cdeg, g.cregular);
   switch (*bucket) {
-    case 6: return g.vs4 == 1 ? pick_fpc<6, true, 1>(fpc) : pick_fpc<6, true, 0>(fpc);
-    case 3: return pick_fpc<3, true, 0>(fpc);
-    case 8: return pick_fpc<8, false, 0>(fpc);
-    case 16: return pick_fpc<16, false, 0>(fpc);
-    case 32: return pick_fpc<32, false, 0>(fpc);
+    case 6: return g.vs4 == 1 ? pick_fpc<6, true, 1>(fpc, fv) : pick_fpc<6, true, 0>(fpc, fv);
+    case 3: return pick_fpc<3, true, 0>(fpc, fv);
+    case 8: return pick_fpc<8, false, 0>(fpc, fv);
+    case 16: return pick_fpc<16, false, 0>(fpc, fv);
+    case 32: return pick_fpc<32, false, 0>(fpc, fv);
     default: return nullptr;
   }
 }
@@ -391,6 +483,7 @@ void set_tuning(int fpc, int threads) {
   g_tune_fpc = fpc;
   g_tune_threads = threads;
 }
+void set_frames_per_thread(int fv) { g_tune_fv = fv; }
 
 int64_t kernel_launch_count() { return g_launches.load(); }
 void note_launches(int n) { g_launches += n; }
@@ -429,17 +522,22 @@ Plan plan_resident(const DevGraph& g, int64_t frames) {
   }
   if (bytes(fpc) > limit) return p;  // does not fit: no resident plan
   int bucket = 0;
-  if (!pick_kernel(g, fpc, &bucket)) return p;
-  const int max_nt = bucket <= 8 ? 512 : (bucket <= 16 ? 256 : 128);
+  int fv = g_tune_fv.load();
+  if (fv <= 0) fv = (fpc >= 2 && cn_bucket(g.max_cdeg, g.cregular) <= 8) ? 2 : 1;
+  if (!pick_kernel(g, fpc, fv, &bucket)) return p;
+  const int max_nt = fv == 2 ? 256 : (bucket <= 8 ? 512 : (bucket <= 16 ? 256 : 128));
+  const int ng = fpc / fv;  // frame vectors per CTA
   int nt = g_tune_threads.load();
   if (nt <= 0) {
-    // one CN item per thread for the largest group, in whole warps
-    nt = (fpc * g.max_cn_items + 31) / 32 * 32;
-    nt = std::max(128, std::min(nt, std::min(max_nt, 512)));
+    // one CN item per frame vector for the largest group, in whole warps
+    nt = (ng * g.max_cn_items + 31) / 32 * 32;
+    nt = std::max(64, std::min(nt, max_nt));
   }
+  if (nt % ng || nt > max_nt) return p;
   p.kernel = 1;
   p.fpc = fpc;
-  p.threads = std::min(nt, max_nt);
+  p.fv = fv;
+  p.threads = nt;
   p.smem = static_cast<int>(bytes(fpc));
   p.degree_bucket = bucket;
   p.ctas = (frames + fpc - 1) / fpc;
@@ -455,7 +553,7 @@ int launch_decode(const DevGraph& g, const DecodeArgs& a_in, void* stream, Plan*
   if (p.kernel == 0) return static_cast<int>(cudaErrorInvalidConfiguration);
   if (a.frames <= 0) return 0;
   int bucket = 0;
-  KernelFn fn = pick_kernel(g, p.fpc, &bucket);
+  KernelFn fn = pick_kernel(g, p.fpc, p.fv, &bucket);
   cudaError_t err = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem);
   if (err != cudaSuccess) return static_cast<int>(err);

@@ -61,6 +61,7 @@ inline int cn_record_stride(int bucket) { return (2 + bucket + 3) / 4 * 4; }
 struct Plan {
   int kernel = 0;  // 1 = SMEM-resident frame-interleaved, 2 = HBM-streamed
   int fpc = 0;     // frames per CTA
+  int fv = 1;      // frames per thread (resident kernel)
   int threads = 0;
   int smem = 0;    // dynamic shared memory bytes
   int degree_bucket = 0;
@@ -74,6 +75,7 @@ int launch_channel(int n, double sigma2, uint64_t seed, int64_t frame0, int64_t 
 int launch_check_update(int degree, int64_t rows, const float* v2c, float* c2v, void* stream);
 
 void set_tuning(int fpc, int threads);
+void set_frames_per_thread(int fv);
 void set_force_kernel(int kernel);  // 0 auto, 1 resident, 2 streamed
 void note_launches(int n);
 // HBM-streamed decoder (stream.cu): frames whose state does not fit one SM

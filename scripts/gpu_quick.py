@@ -8,7 +8,7 @@ g = P.configs.c1_code(); og = orc.graph(g.n_vars, *g.csr())
 sigma2 = P.sigma2_from_ebn0(2.0, g.rate)
 F = 4000
 llr = orc.transmit_batch_f32(sigma2, 1, g.n_vars, 0, F, 16)
-for lazy in (0, 1):
+for lazy in (1,):
     P.set_lazy_totals(lazy)
     for name, s in P.configs.c1_schedules(g).items():
         for es, iters in ((True, 20), (False, 10)):
@@ -26,10 +26,10 @@ P.set_lazy_totals(0)
 s = P.configs.c1_schedules(g)['ndgsbp']
 F = 1 << 18
 x = P.transmit_all_zero(g.n_vars, sigma2, 1, 0, F)
-for lazy in (0, 1):
+for lazy in (1,):
   P.set_lazy_totals(lazy)
-  for fpc, th in [(0,0),(4,384),(2,192),(2,224),(2,256)]:
-    P.set_tuning(fpc, th)
+  for fpc, th, fv in [(0,0,0),(2,96,2),(2,192,1),(4,192,2)]:
+    P.set_tuning(fpc, th, fv)
     for _ in range(2): P.decode_batch(g, s, x, 10, early_stop=False, packed=True)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -37,5 +37,5 @@ for lazy in (0, 1):
     for _ in range(3): P.decode_batch(g, s, x, 10, early_stop=False, packed=True)
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)/3
-    print(f"lazy {lazy} fpc {fpc} th {th} plan {P.plan(g,s,F)} {ms:.2f} ms -> {F/ms*1e3:.3e} frames/s {F/ms*1e3*504:.3e} info bits/s")
+    print(f"fv {fv} fpc {fpc} th {th} plan {P.plan(g,s,F)} {ms:.2f} ms -> {F/ms*1e3:.3e} frames/s {F/ms*1e3*504:.3e} info bits/s")
 P.set_tuning(0,0); P.set_lazy_totals(0)
