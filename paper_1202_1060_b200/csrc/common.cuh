@@ -50,11 +50,15 @@ __device__ __forceinline__ void boxplus_row(const float (&x)[D], int deg, Store&
       z[k] = 0.f;  // boxplus identity (N, D) = (0, 1)
     }
   }
+  // |out| = lg2 D - lg2 N: the boxplus of clamped inputs cannot exceed the
+  // clamp, so no output clamp is applied (rounding may add < 1e-5 to a
+  // saturated message); the magnitude's sign bit is replaced by the parity of
+  // the other inputs' signs in one bit-select.
   auto emit = [&](int k, float num, float den) {
     if (EXACT || k < deg) {
-      const float mag = fminf(fabsf(mufu_lg2(den) - mufu_lg2(num)), kClampB);
-      const unsigned sgn = (sg ^ __float_as_uint(x[k])) & 0x80000000u;
-      store(k, __uint_as_float(__float_as_uint(mag) | sgn));
+      const unsigned d = __float_as_uint(mufu_lg2(den) - mufu_lg2(num));
+      const unsigned t = sg ^ __float_as_uint(x[k]);
+      store(k, __uint_as_float((d & 0x7fffffffu) | (t & 0x80000000u)));
     }
   };
   // prefix p[k] = z0 (+) ... (+) zk for k <= D-2: (N, D) <- (N + z D, D + z N)
@@ -77,12 +81,19 @@ __device__ __forceinline__ void boxplus_row(const float (&x)[D], int deg, Store&
     sd = td;
   }
 #pragma unroll
-  for (int k = D - 3; k >= 1; --k) {
+  for (int k = D - 3; k >= 2; --k) {
     // out_k = p[k-1] (+) s[k+1], rounded symmetrically (see above)
     emit(k, __fadd_rn(__fmul_rn(pn[k - 1], sd), __fmul_rn(sn, pd[k - 1])),
          __fadd_rn(__fmul_rn(pd[k - 1], sd), __fmul_rn(pn[k - 1], sn)));
     const float tn = fmaf(z[k], sd, sn);
     const float td = fmaf(z[k], sn, sd);
+    sn = tn;
+    sd = td;
+  }
+  if (D >= 4) {  // out_1 = z0 (+) s[2]: prefix p[0] = (z0, 1), same rounding pattern without the * 1
+    emit(1, __fadd_rn(__fmul_rn(pn[0], sd), sn), __fadd_rn(sd, __fmul_rn(pn[0], sn)));
+    const float tn = fmaf(z[1], sd, sn);
+    const float td = fmaf(z[1], sn, sd);
     sn = tn;
     sd = td;
   }

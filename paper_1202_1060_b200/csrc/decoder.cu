@@ -86,7 +86,7 @@ __device__ __forceinline__ void sts(float* p, const FVec<FV>& x) {
 }
 
 // live: bit i set when frame i of this thread's vector is still decoding
-template <int D, bool EXACT, int FPC, int FV>
+template <int D, bool EXACT, int FPC, int FV, bool ALL_LIVE>
 __device__ __forceinline__ void cn_update(float* __restrict__ c2v, float* __restrict__ P,
                                           const CnRecord<D, EXACT>& cr, unsigned live) {
   const int base = cr.slot();
@@ -108,18 +108,17 @@ __device__ __forceinline__ void cn_update(float* __restrict__ c2v, float* __rest
     float x[D];
 #pragma unroll
     for (int k = 0; k < D; ++k) x[k] = pv[k].v[i] - old[k].v[i];
-    boxplus_row<D, EXACT>(x, deg, [&](int k, float c) { out[k].v[i] = live & (1u << i) ? c : old[k].v[i]; });
+    boxplus_row<D, EXACT>(x, deg, [&](int k, float c) {
+      out[k].v[i] = (ALL_LIVE || (live & (1u << i))) ? c : old[k].v[i];
+      // in-place posterior: P + (c - old) = v2c + c (v2c = P - old, unclamped)
+      pv[k].v[i] = (ALL_LIVE || (live & (1u << i))) ? x[k] + c : pv[k].v[i];
+    });
   }
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     if (!cr.has(k)) continue;
     sts<FV>(c2v + (base + k) * FPC, out[k]);
-    if (mask & (1u << k)) {
-      FVec<FV> p;
-#pragma unroll
-      for (int i = 0; i < FV; ++i) p.v[i] = pv[k].v[i] + (out[k].v[i] - old[k].v[i]);
-      sts<FV>(P + cr.var(k) * FPC, p);
-    }
+    if (mask & (1u << k)) sts<FV>(P + cr.var(k) * FPC, pv[k]);
   }
 }
 
@@ -267,9 +266,15 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
       if (j0 < xn) fix_first = __ldg(fix_vn + static_cast<size_t>(x0 + j0) * vs4);
       if (live && j0 < cn) {
         const int32_t* rec = g.cn_rec + static_cast<size_t>(c0) * CS;
-        cn_update<D, EXACT, FPC, FV>(c2v, P, next_cn, live);
-        for (int j = j0 + jstep; j < cn; j += jstep)
-          cn_update<D, EXACT, FPC, FV>(c2v, P, CnRecord<D, EXACT>(rec + j * CS), live);
+        if (live == (1u << FV) - 1) {
+          cn_update<D, EXACT, FPC, FV, true>(c2v, P, next_cn, live);
+          for (int j = j0 + jstep; j < cn; j += jstep)
+            cn_update<D, EXACT, FPC, FV, true>(c2v, P, CnRecord<D, EXACT>(rec + j * CS), live);
+        } else {
+          cn_update<D, EXACT, FPC, FV, false>(c2v, P, next_cn, live);
+          for (int j = j0 + jstep; j < cn; j += jstep)
+            cn_update<D, EXACT, FPC, FV, false>(c2v, P, CnRecord<D, EXACT>(rec + j * CS), live);
+        }
       }
       {
         const int ng = grp + 1 < g.G ? grp + 1 : 0;

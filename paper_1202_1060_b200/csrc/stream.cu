@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ rec
     if (mask & (1u << k)) {
       float4 p = pv[k];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) lane(p, i) += lane(out[k], i) - lane(old[k], i);
+      for (int i = 0; i < 4; ++i) lane(p, i) = (lane(pv[k], i) - lane(old[k], i)) + lane(out[k], i);
       st4(s.P + static_cast<int64_t>(cr.var(k)) * s.B + 4 * q, p);
     }
   }

@@ -110,7 +110,7 @@ def test_check_update_saturation(P, torch):
                 if True else 0 for k in range(len(row))]
         want = np.clip(want, -30, 30)
         assert msg_close(g, want) <= 1e-3
-    assert np.all(np.abs(got) <= 30.0)
+    assert np.all(np.abs(got) <= 30.0 * (1 + 1e-6))  # clamped inputs bound the output; rounding only
 
 
 # ------------------------------------------------------- sub-iterations ----
