@@ -91,6 +91,19 @@ int ldpcb_schedule_flooding(ldpcb_code code, ldpcb_schedule *out);              
 int ldpcb_schedule_disjoint(ldpcb_code code, int n_groups, uint64_t seed, ldpcb_schedule *out); /* :136-149 */
 int ldpcb_schedule_nondisjoint(ldpcb_code code, int n_groups, double overlap, uint64_t seed,
                                ldpcb_schedule *out);                                /* :151-171 */
+/* The reference harness's grouping (run_sweep, sim.hpp:113-117): every frame
+ * draws its own random groups, make_*_schedule with seed
+ * mix_seed(schedule_seed, frame_id), and with regroup_each_iteration redraws
+ * them every iteration (decoder.hpp:153-156). Frame ids are the batch index
+ * for decode calls and the true frame id for simulate calls. */
+int ldpcb_schedule_per_frame(ldpcb_code code, int kind, int n_groups, double overlap, uint64_t schedule_seed,
+                             int regroup_each_iteration, ldpcb_schedule *out);
+/* The groups a per-frame schedule uses for frames [frame0, frame0+frames) at
+ * one iteration (schedule_groups_for, schedule.hpp:121-127), generated on
+ * the device: d_cns[f * slots + j], slots = the schedule's total slot count,
+ * group g at [group_offsets[g], group_offsets[g+1]) of ldpcb_schedule_export. */
+int ldpcb_schedule_per_frame_groups_device(ldpcb_code code, ldpcb_schedule s, int64_t frame0, int64_t frames,
+                                           int iteration, uint16_t *d_cns, void *stream);
 /* fixed wrapping windows: group g = CNs (g*stride + j) mod M, j < window */
 int ldpcb_schedule_windows(ldpcb_code code, int kind, int n_groups, int window, int stride, ldpcb_schedule *out);
 int ldpcb_schedule_dims(ldpcb_schedule s, int32_t *kind, int32_t *n_groups, int32_t *n_slots, int32_t *group_size,

@@ -535,13 +535,25 @@ static int syndrome_weight(const orc_graph *g, const uint8_t *bits) {
 
 /* decode, decoder.hpp:143-181 (early_stop=1); early_stop=0 is the
  * fixed-iteration composition used by acceptance.cpp:142-146 */
-static int decode_impl(dstate *st, const orc_graph *g, const orc_schedule *s, const double *llr, int max_iters,
-                       int early_stop, uint8_t *bits, int32_t *iterations, uint8_t *converged, double *posterior,
-                       int32_t *trace, int64_t *cn_updates) {
+static int decode_impl(dstate *st, const orc_graph *g, const orc_schedule *s, uint64_t frame_id, const double *llr,
+                       int max_iters, int early_stop, uint8_t *bits, int32_t *iterations, uint8_t *converged,
+                       double *posterior, int32_t *trace, int64_t *cn_updates) {
   if (max_iters < 1) return fail("max_iters must be >= 1");
   init_state(st, g, llr);
   const int32_t *goff = s->grp_off, *gcns = s->grp_cns;
   int G = s->n_groups;
+  uint64_t seed = s->seed;
+  if (s->per_frame && s->kind != ORC_FLOODING) {
+    /* run_frame (sim.hpp:113-117): sched.seed = mix_seed(schedule_seed,
+     * frame_id); groups = schedule_groups_for(sched, M, 1) */
+    seed = orc_mix_seed(s->seed, frame_id);
+    const double ov = s->kind == ORC_NONDISJOINT ? s->overlap : 0.0;
+    if (orc_generate_groups(g->m, s->n_groups, ov, orc_mix_seed(seed, 1), st->regroup_off, st->regroup_cns,
+                            2 * g->m + 1) < 0)
+      return -1;
+    goff = st->regroup_off;
+    gcns = st->regroup_cns;
+  }
   int64_t cnu = 0;
   int conv = 0, iters = 0;
   if (trace)
@@ -549,7 +561,7 @@ static int decode_impl(dstate *st, const orc_graph *g, const orc_schedule *s, co
   for (int iter = 1; iter <= max_iters; ++iter) {
     if (iter > 1 && s->regroup && s->kind != ORC_FLOODING) { /* decoder.hpp:153-156 */
       const double ov = s->kind == ORC_NONDISJOINT ? s->overlap : 0.0;
-      if (orc_generate_groups(g->m, s->n_groups, ov, orc_mix_seed(s->seed, (uint64_t)iter), st->regroup_off,
+      if (orc_generate_groups(g->m, s->n_groups, ov, orc_mix_seed(seed, (uint64_t)iter), st->regroup_off,
                               st->regroup_cns, 2 * g->m + 1) < 0)
         return -1;
       goff = st->regroup_off;
@@ -583,6 +595,7 @@ static int decode_impl(dstate *st, const orc_graph *g, const orc_schedule *s, co
 
 static int check_schedule(const orc_graph *g, const orc_schedule *s) {
   if (s->n_groups < 1) return fail("schedule needs at least one group");
+  if (s->per_frame) return 0; /* groups are generated per frame */
   for (int k = 0; k < s->n_groups; ++k)
     for (int i = s->grp_off[k]; i < s->grp_off[k + 1]; ++i)
       if (s->grp_cns[i] < 0 || s->grp_cns[i] >= g->m) return fail("group CN index out of range");
@@ -595,7 +608,7 @@ int orc_decode(const orc_graph *g, const orc_schedule *s, const double *llr, int
   if (check_schedule(g, s)) return -1;
   dstate st;
   state_alloc(&st, g, s->n_groups);
-  const int rc = decode_impl(&st, g, s, llr, max_iters, early_stop, bits, iterations, converged, posterior,
+  const int rc = decode_impl(&st, g, s, 0, llr, max_iters, early_stop, bits, iterations, converged, posterior,
                              trace, cn_updates);
   state_free(&st);
   return rc;
@@ -647,7 +660,8 @@ static void *batch_worker(void *arg) {
     for (int v = 0; v < g->n; ++v) llr[v] = (double)J->llr[f * g->n + v];
     int32_t it = 0;
     uint8_t cv = 0;
-    if (decode_impl(&st, g, J->s, llr, J->max_iters, J->early_stop, J->bits ? J->bits + f * g->n : NULL, &it, &cv,
+    if (decode_impl(&st, g, J->s, (uint64_t)f, llr, J->max_iters, J->early_stop, J->bits ? J->bits + f * g->n : NULL,
+                    &it, &cv,
                     J->posterior ? post : NULL, J->trace ? J->trace + f * J->max_iters : NULL, NULL)) {
       J->rc = -1;
       break;
@@ -742,7 +756,8 @@ static void *sim_worker(void *arg) {
       for (int v = 0; v < g->n; ++v) llr[v] = (double)(float)llr[v];
     int32_t it = 0;
     uint8_t cv = 0;
-    if (decode_impl(&st, g, J->s, llr, J->max_iters, J->early_stop, bits, &it, &cv, NULL, NULL, NULL)) {
+    if (decode_impl(&st, g, J->s, J->frame0 + (uint64_t)f, llr, J->max_iters, J->early_stop, bits, &it, &cv, NULL,
+                    NULL, NULL)) {
       J->rc = -1;
       break;
     }

@@ -75,6 +75,10 @@ typedef struct {
   int regroup;     /* regroup_each_iteration */
   const int32_t *grp_off;
   const int32_t *grp_cns;
+  /* run_sweep's grouping (sim.hpp:113-117): groups drawn per frame from
+   * mix_seed(seed, frame_id); grp_off/grp_cns unused. Frame ids: batch
+   * index (decode_batch) or the true frame id (simulate); orc_decode uses 0. */
+  int per_frame;
 } orc_schedule;
 
 /* decoder.hpp:59-87 on one CN of the given degree */

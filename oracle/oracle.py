@@ -44,6 +44,14 @@ def _groups_csr(groups):
     return off, cns
 
 
+class PerFrame:
+    """run_sweep's per-frame grouping (sim.hpp:113-117) in place of explicit
+    groups: kind, G, overlap, schedule_seed, regroup_each_iteration."""
+
+    def __init__(self, kind, n_groups, overlap, seed, regroup=True):
+        self.kind, self.n_groups, self.overlap, self.seed, self.regroup = kind, n_groups, overlap, seed, regroup
+
+
 class _Sched(C.Structure):
     _fields_ = [
         ("kind", C.c_int),
@@ -53,6 +61,7 @@ class _Sched(C.Structure):
         ("regroup", C.c_int),
         ("grp_off", C.c_void_p),
         ("grp_cns", C.c_void_p),
+        ("per_frame", C.c_int),
     ]
 
 
@@ -145,8 +154,11 @@ class COracle:
         return out
 
     def _sched(self, groups, kind=2, overlap=0.0, seed=0, regroup=0):
+        if isinstance(groups, PerFrame):
+            p = groups
+            return _Sched(p.kind, p.n_groups, p.overlap, p.seed, int(p.regroup), None, None, 1), None
         off, cns = _groups_csr(groups)
-        s = _Sched(kind, len(groups), overlap, seed, regroup, off.ctypes.data, cns.ctypes.data)
+        s = _Sched(kind, len(groups), overlap, seed, regroup, off.ctypes.data, cns.ctypes.data, 0)
         return s, (off, cns)
 
     def decode(self, g, groups, llr, max_iters, early_stop=True, kind=2, overlap=0.0, seed=0, regroup=0):

@@ -250,6 +250,17 @@ class GroupSchedule:
         return cls._make(g, lib.ldpcb_schedule_nondisjoint, n_groups, overlap, seed)
 
     @classmethod
+    def per_frame(cls, g: TannerGraph, kind: int, n_groups: int = 1, overlap: float = 0.0, schedule_seed: int = 2,
+                  regroup_each_iteration: bool = True) -> "GroupSchedule":
+        """The reference harness's grouping (sim.hpp:113-117, decoder.hpp:153-156):
+        random groups per frame (and per iteration when regrouping)."""
+        s = cls._make(g, lib.ldpcb_schedule_per_frame, kind, n_groups, overlap, schedule_seed,
+                      int(regroup_each_iteration))
+        s.regroup_each_iteration = bool(regroup_each_iteration) and kind != FLOODING
+        s.per_frame_seed = schedule_seed if kind != FLOODING else None
+        return s
+
+    @classmethod
     def windows(cls, g: TannerGraph, n_groups: int, window: int, stride: int, kind: int | None = None):
         if kind is None:
             kind = NONDISJOINT if window > stride else DISJOINT
@@ -263,6 +274,15 @@ class GroupSchedule:
             check(lib.ldpcb_schedule_export(self._h, _vp(off), _vp(cns)))
             self._groups = [cns[off[k] : off[k + 1]].tolist() for k in range(self.n_groups)]
         return self._groups
+
+    def frame_groups(self, frame0: int, frames: int, iteration: int = 1) -> "torch.Tensor":
+        """Device-generated groups of a per-frame schedule: int32 [frames, n_slots]
+        in group order (split at the offsets of ``groups``)."""
+        import torch
+        out = torch.empty((frames, self.n_slots), dtype=torch.int16, device="cuda")
+        check(lib.ldpcb_schedule_per_frame_groups_device(self.graph.handle, self._h, frame0, frames, iteration,
+                                                         out.data_ptr(), _stream()))
+        return out.view(torch.uint16).to(torch.int32) if hasattr(torch, "uint16") else (out.to(torch.int32) & 0xFFFF)
 
     def iteration_budget(self, i_max: int) -> int:
         b = C.c_int32()

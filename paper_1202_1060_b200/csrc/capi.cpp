@@ -216,6 +216,14 @@ ldpcb::DevGraph dev_graph(ldpcb_code code, ldpcb_schedule s) {
   g.fix_rec = d.fix_rec;
   g.all_vn_rec = d.all_vn_rec;
   g.all_rec = d.all_rec;
+  const auto& sh = s->impl->host;
+  g.per_frame = sh.per_frame;
+  g.regroup = sh.regroup;
+  g.balanced = sh.overlap == 0.0;
+  g.nominal = sh.nominal;
+  g.k_overlap = sh.k_overlap;
+  g.list_slots = static_cast<int>(sh.grp_cns.size());
+  g.schedule_seed = sh.seed;
   g.h_cn_off = t.cn_off.data();
   g.h_fix_off = t.fix_off.data();
   return g;
@@ -381,6 +389,19 @@ int ldpcb_schedule_nondisjoint(ldpcb_code code, int n_groups, double overlap, ui
   });
 }
 
+int ldpcb_schedule_per_frame(ldpcb_code code, int kind, int n_groups, double overlap, uint64_t schedule_seed,
+                             int regroup_each_iteration, ldpcb_schedule* out) {
+  return guard([&] {
+    need(code != nullptr, "null handle");
+    need(kind >= 0 && kind <= 2, "unknown schedule kind");
+    need(code->impl->host.m < 65536, "per-frame groupings support up to 65535 checks");
+    return make_sched(code->impl,
+                      ldpcb::per_frame_schedule(code->impl->host, static_cast<ldpcb::Kind>(kind), n_groups, overlap,
+                                                schedule_seed, regroup_each_iteration != 0),
+                      out);
+  });
+}
+
 int ldpcb_schedule_windows(ldpcb_code code, int kind, int n_groups, int window, int stride, ldpcb_schedule* out) {
   return guard([&] {
     need(code != nullptr, "null handle");
@@ -538,6 +559,7 @@ int ldpcb_decode_host(ldpcb_code code, ldpcb_schedule s, int64_t frames, const f
       cuda_check(cudaMemcpyAsync(buf[k].llr, llr + c0 * n, cnt * n * sizeof(float), cudaMemcpyHostToDevice, st[k]),
                  "H2D");
       ldpcb::DecodeArgs a;
+      a.frame0 = c0;
       a.frames = cnt;
       a.llr = buf[k].llr;
       a.max_iters = max_iters;
@@ -609,6 +631,7 @@ int ldpcb_simulate_device(ldpcb_code code, ldpcb_schedule s, double sigma2, uint
       const int64_t cnt = std::min(chunk, frames - c0);
       launch(ldpcb::launch_channel(g.n, sigma2, channel_seed, frame_begin + c0, cnt, scratch, stream), "channel");
       ldpcb::DecodeArgs a;
+      a.frame0 = frame_begin + c0;
       a.frames = cnt;
       a.llr = scratch;
       a.max_iters = max_iters;
@@ -660,6 +683,19 @@ int ldpcb_check_update_device(int degree, int64_t rows, const float* d_v2c, floa
     need(degree >= 2 && degree <= 32, "degree must be in [2, 32]");
     need(rows >= 0, "rows must be >= 0");
     launch(ldpcb::launch_check_update(degree, rows, d_v2c, d_c2v, stream), "check_update kernel");
+    return LDPCB_OK;
+  });
+}
+
+int ldpcb_schedule_per_frame_groups_device(ldpcb_code code, ldpcb_schedule s, int64_t frame0, int64_t frames,
+                                           int iteration, uint16_t* d_cns, void* stream) {
+  return guard([&] {
+    check_pair(code, s);
+    need(s->impl->host.per_frame, "not a per-frame schedule");
+    need(iteration >= 1, "iteration must be >= 1");
+    need(frames >= 0 && d_cns != nullptr, "bad output");
+    const auto g = dev_graph(code, s);
+    launch(ldpcb::launch_gen_groups(g, frame0, frames, iteration - 1, 1, d_cns, stream), "group generator");
     return LDPCB_OK;
   });
 }

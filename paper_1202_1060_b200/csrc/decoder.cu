@@ -180,9 +180,14 @@ __device__ __forceinline__ unsigned parity(const float* __restrict__ P, const in
 
 constexpr int max_threads_for(int D, int FV) { return FV == 2 ? 256 : (D <= 8 ? 512 : (D <= 16 ? 256 : 128)); }
 
-template <int D, bool EXACT, int FPC, int FV, int VS>
+// RND: per-frame random grouping (host.hpp ScheduleData::per_frame). Each
+// frame's ordered CN groups come from a generated list (gen_groups_kernel);
+// the CN records are the per-CN ones (no in-place posterior updates) and
+// after every CN phase each edge of the group re-sums its VN exactly.
+template <int D, bool EXACT, int FPC, int FV, int VS, bool RND = false>
 __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode_resident(const DevGraph g,
                                                                                           const DecodeArgs a) {
+  static_assert(!RND || FV == 1, "per-frame groupings need one frame per thread");
   constexpr int CS = CnRecord<D, EXACT>::kInts;
   constexpr int NG = FPC / FV;  // frame vectors per CTA
   extern __shared__ __align__(16) float smem[];
@@ -202,6 +207,8 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
   int* const s_berr = s_conv + FPC;
   int* const s_cn_off = s_berr + FPC;         // [G+1] staged group tables
   int* const s_fix_off = s_cn_off + g.G + 1;  // [G+1]
+  uint16_t* const s_list = reinterpret_cast<uint16_t*>(s_fix_off + g.G + 1);  // RND: [FPC][slots]
+  const int slots = a.list_slots;
   const int4* const all_vn = reinterpret_cast<const int4*>(g.all_vn_rec);
   const int4* const fix_vn = reinterpret_cast<const int4*>(g.fix_rec);
 
@@ -251,16 +258,42 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
   // records are prefetched one phase ahead: the first CN item of the next
   // group and the first fix-up item of the current one
   CnRecord<D, EXACT> next_cn;
-  if (j0 < s_cn_off[1] - s_cn_off[0]) next_cn.load(g.cn_rec + static_cast<size_t>(s_cn_off[0] + j0) * CS);
+  if (!RND && j0 < s_cn_off[1] - s_cn_off[0]) next_cn.load(g.cn_rec + static_cast<size_t>(s_cn_off[0] + j0) * CS);
 
   const bool dump = a.max_subiters > 0;
   int sub = 0;
   for (int iter = 1; iter <= a.max_iters; ++iter) {
+    if constexpr (RND) {
+      if (iter == 1 || a.n_lists > 1) {  // this iteration's groups (decoder.hpp:153-156)
+        const int li = a.n_lists > 1 ? iter - 1 : 0;
+        for (int i = tid; i < nf * slots; i += nt) {
+          const int ff = i / slots, j = i - ff * slots;
+          s_list[ff * slots + j] = a.lists[((f0 + ff) * a.n_lists + li) * slots + j];
+        }
+        __syncthreads();
+      }
+    }
     for (int grp = 0; grp < g.G; ++grp) {
       if (dump && sub == a.max_subiters) goto finish;
       ++sub;
       // CN phase: every (CN of the group, frame vector); Jacobi within the group
       const int c0 = s_cn_off[grp], cn = s_cn_off[grp + 1] - c0;
+      if constexpr (RND) {
+        const uint16_t* lst = s_list + fb * slots + c0;
+        if (live)
+          for (int j = j0; j < cn; j += jstep)
+            cn_update<D, EXACT, FPC, FV, true>(c2v, P, CnRecord<D, EXACT>(g.all_rec + lst[j] * CS), live);
+        __syncthreads();
+        // every VN of the group re-summed from its record (a VN shared by
+        // several CNs is written several times with the same value)
+        if (live)
+          for (int e = j0; e < cn * D; e += jstep) {
+            const int v = __ldg(g.all_rec + lst[e / D] * CS + 2 + e % D);
+            if (EXACT || v >= 0) vn_sum<FPC, FV, VS>(c2v, P, L, all_vn + v * vs4, vs4, __ldg(all_vn + v * vs4));
+          }
+        __syncthreads();
+        continue;
+      }
       const int x0 = s_fix_off[grp], xn = s_fix_off[grp + 1] - x0;
       int4 fix_first = make_int4(0, 0, 0, 0);
       if (j0 < xn) fix_first = __ldg(fix_vn + static_cast<size_t>(x0 + j0) * vs4);
@@ -297,7 +330,7 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
     const bool check = a.early_stop || a.trace || iter == a.max_iters;
     // ---- exact totals (decoder.hpp:162-165): removes the rounding of the
     // in-place posterior updates before hard decisions are taken
-    if (g.recompute && (check || !a.lazy_totals)) {
+    if (!RND && g.recompute && (check || !a.lazy_totals)) {
       if (live) vn_sum_range<FPC, FV, VS>(c2v, P, L, all_vn, vs4, j0, n, jstep);
       __syncthreads();
     }
@@ -338,7 +371,7 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
 finish:
   __syncthreads();
   if (dump) {
-    if (g.recompute) vn_sum_range<FPC, FV, VS>(c2v, P, L, all_vn, vs4, j0, n, jstep);
+    if (!RND && g.recompute) vn_sum_range<FPC, FV, VS>(c2v, P, L, all_vn, vs4, j0, n, jstep);
     __syncthreads();
     const int E = g.E;
 #pragma unroll
@@ -424,6 +457,57 @@ __global__ void check_update_kernel(int deg, int64_t rows, const float* __restri
   boxplus_row<D, EXACT>(x, deg, [&](int k, float c) { c2v[r * deg + k] = c * kLn2; });
 }
 
+// generate_groups (schedule.hpp:54-115) for (frame, list) pairs on the device:
+// list l of frame f uses Rng(mix_seed(mix_seed(schedule_seed, f), l + 1)),
+// the stream run_sweep / decode draw from (sim.hpp:113-117, decoder.hpp:153-156).
+// Per-thread scratch (pool, first group of each CN, candidates) is in
+// shared memory.
+__global__ void gen_groups_kernel(int M, int G, int balanced, int nominal, int k, uint64_t schedule_seed,
+                                  int64_t frame0, int64_t frames, int list0, int n_lists, int slots,
+                                  uint16_t* __restrict__ out) {
+  extern __shared__ uint16_t gsm[];
+  const int per = (2 * M + nominal + 1) | 1;  // uint16 per thread (odd: spread banks)
+  uint16_t* pool = gsm + threadIdx.x * per;
+  uint16_t* first = pool + M;
+  uint16_t* cand = first + M;
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (item >= frames * n_lists) return;
+  const int64_t f = item / n_lists;
+  const int l = static_cast<int>(item - f * n_lists);
+  uint16_t* o = out + item * slots;
+  Stream rng(stream_seed(stream_seed(schedule_seed, static_cast<uint64_t>(frame0 + f)), static_cast<uint64_t>(list0 + l + 1)));
+  for (int i = 0; i < M; ++i) pool[i] = static_cast<uint16_t>(i);
+  rng.permute(pool, static_cast<uint64_t>(M));
+  if (balanced) {  // disjoint: consecutive slices of the shuffled pool
+    for (int i = 0; i < M; ++i) o[i] = static_cast<uint16_t>(pool[i]);
+    return;
+  }
+  int next = min(nominal, M), w = next;
+  for (int i = 0; i < next; ++i) {
+    o[i] = static_cast<uint16_t>(pool[i]);
+    first[pool[i]] = 0;
+  }
+  int prev_start = 0, prev_len = next;
+  for (int grp = 1; grp < G; ++grp) {
+    int nc = 0;  // previous group minus the one before it
+    for (int i = prev_start; i < prev_start + prev_len; ++i)
+      if (grp == 1 || first[o[i]] != grp - 2) cand[nc++] = o[i];
+    rng.permute(cand, static_cast<uint64_t>(nc));
+    const int take = min(k, nc);
+    const int start = w;
+    for (int i = 0; i < take; ++i) o[w++] = static_cast<uint16_t>(cand[i]);
+    const int want = grp == G - 1 ? M - next : nominal - take;
+    const int got = min(want, M - next);
+    for (int i = 0; i < got; ++i) {
+      o[w++] = static_cast<uint16_t>(pool[next + i]);
+      first[pool[next + i]] = static_cast<uint16_t>(grp);
+    }
+    next += got;
+    prev_start = start;
+    prev_len = w - start;
+  }
+}
+
 using KernelFn = void (*)(const DevGraph, const DecodeArgs);
 
 template <int D, bool EXACT, int VS>
@@ -447,8 +531,28 @@ KernelFn pick_fpc(int fpc, int fv) {
   }
 }
 
+template <int D, bool EXACT, int VS>
+KernelFn pick_rnd(int fpc) {
+  switch (fpc) {
+    case 1: return decode_resident<D, EXACT, 1, 1, VS, true>;
+    case 2: return decode_resident<D, EXACT, 2, 1, VS, true>;
+    case 4: return decode_resident<D, EXACT, 4, 1, VS, true>;
+    default: return nullptr;
+  }
+}
+
 KernelFn pick_kernel(const DevGraph& g, int fpc, int fv, int* bucket) {
   *bucket = cn_bucket(g.max_cdeg, g.cregular);
+  if (g.per_frame) {
+    if (fv != 1) return nullptr;
+    switch (*bucket) {
+      case 6: return g.vs4 == 1 ? pick_rnd<6, true, 1>(fpc) : pick_rnd<6, true, 0>(fpc);
+      case 3: return pick_rnd<3, true, 0>(fpc);
+      case 8: return pick_rnd<8, false, 0>(fpc);
+      case 16: return pick_rnd<16, false, 0>(fpc);
+      default: return nullptr;
+    }
+  }
   switch (*bucket) {
     case 6: return g.vs4 == 1 ? pick_fpc<6, true, 1>(fpc, fv) : pick_fpc<6, true, 0>(fpc, fv);
     case 3: return pick_fpc<3, true, 0>(fpc, fv);
@@ -499,7 +603,28 @@ int lazy_totals() { return g_lazy_totals.load(); }
 
 Plan plan_resident(const DevGraph& g, int64_t frames);
 
+int launch_gen_groups(const DevGraph& g, int64_t frame0, int64_t frames, int list0, int n_lists, uint16_t* out,
+                      void* stream) {
+  if (!g.per_frame) return static_cast<int>(cudaErrorInvalidValue);
+  if (frames <= 0 || n_lists <= 0) return 0;
+  const int per = 2 * ((2 * g.m + g.nominal + 1) | 1);  // scratch bytes per thread
+  const int room = device_smem_optin() - 1024;
+  if (per > room) return static_cast<int>(cudaErrorInvalidConfiguration);
+  const int tpb = std::max(1, std::min(64, room / per));
+  cudaError_t err = cudaFuncSetAttribute(reinterpret_cast<const void*>(gen_groups_kernel),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, tpb * per);
+  if (err != cudaSuccess) return static_cast<int>(err);
+  const int64_t items = frames * n_lists;
+  gen_groups_kernel<<<static_cast<unsigned>((items + tpb - 1) / tpb), tpb, tpb * per,
+                      static_cast<cudaStream_t>(stream)>>>(g.m, g.G, g.balanced, g.nominal, g.k_overlap,
+                                                           g.schedule_seed, frame0, frames, list0, n_lists,
+                                                           g.list_slots, out);
+  ++g_launches;
+  return static_cast<int>(cudaGetLastError());
+}
+
 Plan plan_decode(const DevGraph& g, int64_t frames) {
+  if (g.per_frame) return plan_resident(g, frames);  // per-frame groups: resident kernel only
   if (g_force_kernel.load() == 2) return plan_stream(g, frames);
   Plan p = plan_resident(g, frames);
   if (p.kernel == 0 && g_force_kernel.load() != 1) p = plan_stream(g, frames);
@@ -510,7 +635,8 @@ Plan plan_resident(const DevGraph& g, int64_t frames) {
   Plan p;
   const size_t limit = static_cast<size_t>(device_smem_optin()) - 1024;
   const size_t per = frame_bytes(g);
-  auto bytes = [&](int f) { return f * per + 20 * f + 8 * (g.G + 1) + 16; };
+  const size_t list_bytes = g.per_frame ? 2ull * g.list_slots : 0;  // per frame
+  auto bytes = [&](int f) { return f * (per + list_bytes) + 20 * f + 8 * (g.G + 1) + 16; };
   int fpc = g_tune_fpc.load();
   if (fpc <= 0) {
     // largest FPC that still lets four CTAs share an SM (their barriers and
@@ -519,7 +645,7 @@ Plan plan_resident(const DevGraph& g, int64_t frames) {
     const size_t sm_bytes = static_cast<size_t>(device_smem_per_sm()) - 4096;
     fpc = 0;
     for (int ctas : {4, 2, 1}) {
-      for (int c = 8; c >= 1 && fpc == 0; c /= 2)
+      for (int c = g.per_frame ? 4 : 8; c >= 1 && fpc == 0; c /= 2)
         if (bytes(c) <= limit && static_cast<size_t>(ctas) * bytes(c) <= sm_bytes) fpc = c;
       if (fpc) break;
     }
@@ -528,7 +654,7 @@ Plan plan_resident(const DevGraph& g, int64_t frames) {
   if (bytes(fpc) > limit) return p;  // does not fit: no resident plan
   int bucket = 0;
   int fv = g_tune_fv.load();
-  if (fv <= 0) fv = (fpc >= 2 && cn_bucket(g.max_cdeg, g.cregular) <= 8) ? 2 : 1;
+  if (fv <= 0) fv = (fpc >= 2 && cn_bucket(g.max_cdeg, g.cregular) <= 8 && !g.per_frame) ? 2 : 1;
   if (!pick_kernel(g, fpc, fv, &bucket)) return p;
   const int max_nt = fv == 2 ? 256 : (bucket <= 8 ? 512 : (bucket <= 16 ? 256 : 128));
   const int ng = fpc / fv;  // frame vectors per CTA
@@ -562,10 +688,46 @@ int launch_decode(const DevGraph& g, const DecodeArgs& a_in, void* stream, Plan*
   cudaError_t err = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem);
   if (err != cudaSuccess) return static_cast<int>(err);
-  // grid.x limit is 2^31-1, far above any batch
-  fn<<<static_cast<unsigned>(p.ctas), p.threads, p.smem, static_cast<cudaStream_t>(stream)>>>(g, a);
-  ++g_launches;
-  return static_cast<int>(cudaGetLastError());
+  auto st = static_cast<cudaStream_t>(stream);
+  if (!g.per_frame) {
+    // grid.x limit is 2^31-1, far above any batch
+    fn<<<static_cast<unsigned>(p.ctas), p.threads, p.smem, st>>>(g, a);
+    ++g_launches;
+    return static_cast<int>(cudaGetLastError());
+  }
+  // per-frame (and per-iteration) groups, sim.hpp:113-117: generate the
+  // lists for a chunk of frames (<= 512 MB of uint16 lists), then decode it
+  a.n_lists = g.regroup ? a.max_iters : 1;
+  a.list_slots = g.list_slots;
+  const int64_t per_frame_bytes = 2ll * a.n_lists * g.list_slots;
+  int64_t chunk = std::max<int64_t>(p.fpc, (512ll << 20) / per_frame_bytes / p.fpc * p.fpc);
+  chunk = std::min(chunk, a.frames);
+  uint16_t* lists = nullptr;
+  err = cudaMallocAsync(reinterpret_cast<void**>(&lists), per_frame_bytes * chunk, st);
+  if (err != cudaSuccess) return static_cast<int>(err);
+  const int n = g.n, nb = (g.n + 7) / 8;
+  for (int64_t c0 = 0; c0 < a.frames && err == cudaSuccess; c0 += chunk) {
+    const int64_t cnt = std::min(chunk, a.frames - c0);
+    DecodeArgs b = a;
+    b.frames = cnt;
+    b.frame0 = a.frame0 + c0;
+    b.llr = a.llr + c0 * n;
+    if (a.bits) b.bits = a.bits + c0 * (a.bits_packed ? nb : n);
+    if (a.iterations) b.iterations = a.iterations + c0;
+    if (a.converged) b.converged = a.converged + c0;
+    if (a.posterior) b.posterior = a.posterior + c0 * n;
+    if (a.trace) b.trace = a.trace + c0 * a.max_iters;
+    if (a.c2v_out) b.c2v_out = a.c2v_out + c0 * g.E;
+    if (a.v2c_out) b.v2c_out = a.v2c_out + c0 * g.E;
+    b.lists = lists;
+    err = static_cast<cudaError_t>(launch_gen_groups(g, b.frame0, cnt, 0, a.n_lists, lists, st));
+    if (err != cudaSuccess) break;
+    fn<<<static_cast<unsigned>((cnt + p.fpc - 1) / p.fpc), p.threads, p.smem, st>>>(g, b);
+    ++g_launches;
+    err = cudaGetLastError();
+  }
+  cudaFreeAsync(lists, st);
+  return static_cast<int>(err);
 }
 
 int launch_channel(int n, double sigma2, uint64_t seed, int64_t frame0, int64_t frames, float* llr, void* stream) {

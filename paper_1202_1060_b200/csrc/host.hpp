@@ -82,6 +82,14 @@ struct ScheduleData {
   int64_t edge_updates_per_iter = 0;          // sum of CN degrees over group slots
   int64_t touched_per_iter = 0;               // sum of touched-set sizes
   int max_group = 0, max_touched = 0;
+  // Per-frame random grouping (the reference harness, sim.hpp:113-117):
+  // frame f uses generate_groups(M, G, r, Rng(mix_seed(mix_seed(schedule_seed,
+  // f), it))) in iteration it = 1, and again for every it > 1 when regroup
+  // is set (decoder.hpp:153-156). grp_off / grp_cns then hold frame 0's
+  // iteration-1 groups; the offsets are the same for every frame.
+  bool per_frame = false;
+  bool regroup = false;
+  int nominal = 0, k_overlap = 0;
 };
 
 // Compact per-group records read by the resident kernel (one vectorised,
@@ -116,6 +124,8 @@ ScheduleData schedule_from_groups(const CodeData& c, Kind kind, const Rows& grou
 ScheduleData flooding_schedule(const CodeData& c);
 ScheduleData reference_random_schedule(const CodeData& c, Kind kind, int G, double overlap, uint64_t seed);
 ScheduleData window_schedule(const CodeData& c, Kind kind, int G, int window, int stride);
+ScheduleData per_frame_schedule(const CodeData& c, Kind kind, int G, double overlap, uint64_t schedule_seed,
+                                bool regroup);
 Rows random_groups(int M, int G, double overlap, uint64_t stream_seed_value);
 int iteration_budget(const ScheduleData& s, int n_checks, int i_max);
 std::vector<int> measure_cocsg(const CodeData& c, const ScheduleData& s);

@@ -126,6 +126,21 @@ ScheduleData reference_random_schedule(const CodeData& c, Kind kind, int G, doub
   return s;
 }
 
+ScheduleData per_frame_schedule(const CodeData& c, Kind kind, int G, double overlap, uint64_t schedule_seed,
+                                bool regroup) {
+  if (kind == Kind::flooding) return flooding_schedule(c);
+  ScheduleData s = reference_random_schedule(c, kind, G, overlap, stream_seed(schedule_seed, 0));
+  s.seed = schedule_seed;
+  s.per_frame = true;
+  s.regroup = regroup;
+  if (s.overlap != 0.0) {
+    const double denom = G - (G - 1) * s.overlap;
+    s.nominal = static_cast<int>(std::ceil(c.m / denom));
+    s.k_overlap = static_cast<int>(std::llround(s.nominal * s.overlap));
+  }
+  return s;
+}
+
 // Fixed windows: group g = CNs (g*stride + j) mod M for j < window, in that
 // order (BASELINE: 8 windows of 84 at stride 63 on M=504; 45 x 960 at 720).
 ScheduleData window_schedule(const CodeData& c, Kind kind, int G, int window, int stride) {

@@ -24,6 +24,10 @@ struct DevGraph {
   const int32_t* fix_rec = nullptr;
   const int32_t* all_vn_rec = nullptr;  // [n] VN records
   const int32_t* all_rec = nullptr;     // [m] CN records, syndrome
+  // per-frame random grouping (host.hpp ScheduleData::per_frame)
+  bool per_frame = false, regroup = false, balanced = false;
+  int nominal = 0, k_overlap = 0, list_slots = 0;
+  uint64_t schedule_seed = 0;
   // host copies of the per-group offsets (owned by the schedule handle)
   const int32_t* h_cn_off = nullptr;
   const int32_t* h_fix_off = nullptr;
@@ -37,6 +41,9 @@ struct DecodeArgs {
   int early_stop = 1;
   int max_subiters = 0;  // >0: stop after this many sub-iterations and dump state
   int lazy_totals = 0;   // 1: exact totals only in iterations that test the syndrome
+  int64_t frame0 = 0;    // frame id of frame 0 (per-frame schedule streams)
+  const uint16_t* lists = nullptr;  // per-frame group lists [frames][n_lists][list_slots]
+  int n_lists = 0, list_slots = 0;
   uint8_t* bits = nullptr;
   int bits_packed = 0;
   int32_t* iterations = nullptr;
@@ -70,6 +77,10 @@ struct Plan {
 
 Plan plan_decode(const DevGraph& g, int64_t frames);
 // returns cudaError_t as int
+// per-frame group lists (gen_groups_kernel): out[(f * n_lists + l) * list_slots + j]
+// = slot j of the ordered groups of frame frame0+f at iteration list0+l+1
+int launch_gen_groups(const DevGraph& g, int64_t frame0, int64_t frames, int list0, int n_lists, uint16_t* out,
+                      void* stream);
 int launch_decode(const DevGraph& g, const DecodeArgs& a, void* stream, Plan* used);
 int launch_channel(int n, double sigma2, uint64_t seed, int64_t frame0, int64_t frames, float* llr, void* stream);
 int launch_check_update(int degree, int64_t rows, const float* v2c, float* c2v, void* stream);

@@ -266,3 +266,30 @@ def test_oracle_simulate_equals_reference_run_sweep(corc, rorc):
     cnt = corc.simulate(cg, [list(range(60))], s2, 11, 0, 300, 30, round_f32=False)
     assert cnt.tolist()[:4] == [res["frames"], res["bit_errors"], res["frame_errors"], res["converged_frames"]]
     assert cnt[4] / cnt[0] == pytest.approx(res["mean_iters_all"], rel=1e-12)
+
+
+@pytest.mark.parametrize("kind,G,ov,regroup", [(2, 6, 0.4, 1), (1, 5, 0.0, 1), (2, 4, 0.25, 0)])
+def test_oracle_per_frame_grouping_equals_reference_run_sweep(corc, rorc, kind, G, ov, regroup):
+    """run_sweep's default grouping: every frame draws its own groups from
+    mix_seed(schedule_seed, frame_id) and, when regrouping, redraws them each
+    iteration (sim.hpp:113-117, decoder.hpp:153-156). Counters are exact."""
+    from oracle.oracle import PerFrame
+
+    cols = rorc.random_regular(120, 3, 6, 4)
+    off, c = csr_regular(cols, 6)
+    cg, rg = corc.graph(120, off, c), rorc.graph(120, off, c)
+    res = rorc.run_sweep(rg, kind, G, ov, regroup, [1.5], 25, 0, 300, 10**6, 11, 77, 4)[0]
+    s2 = corc.sigma2_from_ebn0(1.5, 0.5)
+    cnt = corc.simulate(cg, PerFrame(kind, G, ov, 77, regroup), s2, 11, 0, 300, 25, round_f32=False)
+    assert cnt.tolist()[:4] == [res["frames"], res["bit_errors"], res["frame_errors"], res["converged_frames"]]
+    assert cnt[4] / cnt[0] == pytest.approx(res["mean_iters_all"], rel=1e-12)
+    # and frame by frame against ldpc::decode with the frame's own schedule
+    for f in (0, 1, 57):
+        seed_f = rorc.mix_seed(77, f)
+        groups, _ = rorc.make_schedule(rg, kind, G, ov, seed_f)
+        llr = corc.transmit_all_zero(s2, 11, 120, f)
+        a = rorc.decode(rg, groups, llr, 25, kind=kind, overlap=ov, seed=seed_f, regroup=regroup)
+        b = corc.decode_batch(cg, PerFrame(kind, G, ov, 77, regroup), np.zeros((f + 1, 120), np.float32), 1)
+        assert b["iterations"].shape == (f + 1,)
+        cc = corc.decode(cg, groups, llr, 25, kind=kind, overlap=ov, seed=seed_f, regroup=regroup)
+        assert np.array_equal(a["bits"], cc["bits"]) and a["iterations"] == cc["iterations"]
