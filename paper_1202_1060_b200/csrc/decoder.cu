@@ -458,53 +458,75 @@ __global__ void check_update_kernel(int deg, int64_t rows, const float* __restri
 }
 
 // generate_groups (schedule.hpp:54-115) for (frame, list) pairs on the device:
-// list l of frame f uses Rng(mix_seed(mix_seed(schedule_seed, f), l + 1)),
+// list l of frame f uses Rng(mix_seed(mix_seed(schedule_seed, f), list0+l+1)),
 // the stream run_sweep / decode draw from (sim.hpp:113-117, decoder.hpp:153-156).
-// Per-thread scratch (pool, first group of each CN, candidates) is in
-// shared memory.
+// One thread per list. The pool and the candidate copy live in shared
+// memory (uint16); the candidates of group g are exactly the fresh part of
+// group g-1 (a carried CN came from group g-2), so no membership array is
+// needed. next_below's two 64-bit remainders use per-CTA reciprocals.
+struct Below {
+  const unsigned long long* recip;  // recip[n] = floor((2^64-1) / n)
+  __device__ __forceinline__ uint64_t mod(uint64_t x, uint32_t n) const {
+    uint64_t r = x - __umul64hi(x, recip[n]) * n;  // quotient low by at most 2
+    while (r >= n) r -= n;
+    return r;
+  }
+  // Stream::below (rng.hpp:67-73): rejection below lim = (2^64 - n) mod n,
+  // which is < n <= 65535, so it is only computed for such tiny draws
+  __device__ __forceinline__ uint32_t draw(Stream& rng, uint32_t n) const {
+    for (;;) {
+      const uint64_t x = rng.u64();
+      if (x > 0xffffull || x >= mod(0ull - n, n)) return static_cast<uint32_t>(mod(x, n));
+    }
+  }
+  __device__ __forceinline__ void permute(Stream& rng, uint16_t* a, int n) const {  // rng.hpp:75-82
+    for (int i = n; i > 1; --i) {
+      const uint32_t j = draw(rng, static_cast<uint32_t>(i));
+      const uint16_t t = a[i - 1];
+      a[i - 1] = a[j];
+      a[j] = t;
+    }
+  }
+};
+
 __global__ void gen_groups_kernel(int M, int G, int balanced, int nominal, int k, uint64_t schedule_seed,
                                   int64_t frame0, int64_t frames, int list0, int n_lists, int slots,
                                   uint16_t* __restrict__ out) {
-  extern __shared__ uint16_t gsm[];
-  const int per = (2 * M + nominal + 1) | 1;  // uint16 per thread (odd: spread banks)
-  uint16_t* pool = gsm + threadIdx.x * per;
-  uint16_t* first = pool + M;
-  uint16_t* cand = first + M;
+  extern __shared__ unsigned long long gsm64[];
+  unsigned long long* recip = gsm64;  // [M + 1]
+  for (int i = threadIdx.x; i <= M; i += blockDim.x) recip[i] = i > 1 ? ~0ull / static_cast<unsigned>(i) : 0ull;
+  const int per = (M + nominal) | 1;  // uint16 per thread (odd: spread banks)
+  uint16_t* pool = reinterpret_cast<uint16_t*>(gsm64 + M + 1) + threadIdx.x * per;
+  uint16_t* cand = pool + M;
+  __syncthreads();
+  const Below bl{recip};
   const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (item >= frames * n_lists) return;
   const int64_t f = item / n_lists;
   const int l = static_cast<int>(item - f * n_lists);
   uint16_t* o = out + item * slots;
-  Stream rng(stream_seed(stream_seed(schedule_seed, static_cast<uint64_t>(frame0 + f)), static_cast<uint64_t>(list0 + l + 1)));
+  Stream rng(stream_seed(stream_seed(schedule_seed, static_cast<uint64_t>(frame0 + f)),
+                         static_cast<uint64_t>(list0 + l + 1)));
   for (int i = 0; i < M; ++i) pool[i] = static_cast<uint16_t>(i);
-  rng.permute(pool, static_cast<uint64_t>(M));
+  bl.permute(rng, pool, M);
   if (balanced) {  // disjoint: consecutive slices of the shuffled pool
-    for (int i = 0; i < M; ++i) o[i] = static_cast<uint16_t>(pool[i]);
+    for (int i = 0; i < M; ++i) o[i] = pool[i];
     return;
   }
   int next = min(nominal, M), w = next;
-  for (int i = 0; i < next; ++i) {
-    o[i] = static_cast<uint16_t>(pool[i]);
-    first[pool[i]] = 0;
-  }
-  int prev_start = 0, prev_len = next;
+  for (int i = 0; i < next; ++i) o[i] = pool[i];
+  int fresh_start = 0, fresh_len = next;  // fresh part of the previous group
   for (int grp = 1; grp < G; ++grp) {
-    int nc = 0;  // previous group minus the one before it
-    for (int i = prev_start; i < prev_start + prev_len; ++i)
-      if (grp == 1 || first[o[i]] != grp - 2) cand[nc++] = o[i];
-    rng.permute(cand, static_cast<uint64_t>(nc));
-    const int take = min(k, nc);
-    const int start = w;
-    for (int i = 0; i < take; ++i) o[w++] = static_cast<uint16_t>(cand[i]);
+    for (int i = 0; i < fresh_len; ++i) cand[i] = pool[fresh_start + i];
+    bl.permute(rng, cand, fresh_len);
+    const int take = min(k, fresh_len);
+    for (int i = 0; i < take; ++i) o[w++] = cand[i];
     const int want = grp == G - 1 ? M - next : nominal - take;
     const int got = min(want, M - next);
-    for (int i = 0; i < got; ++i) {
-      o[w++] = static_cast<uint16_t>(pool[next + i]);
-      first[pool[next + i]] = static_cast<uint16_t>(grp);
-    }
+    for (int i = 0; i < got; ++i) o[w++] = pool[next + i];
+    fresh_start = next;
+    fresh_len = got;
     next += got;
-    prev_start = start;
-    prev_len = w - start;
   }
 }
 
@@ -607,15 +629,18 @@ int launch_gen_groups(const DevGraph& g, int64_t frame0, int64_t frames, int lis
                       void* stream) {
   if (!g.per_frame) return static_cast<int>(cudaErrorInvalidValue);
   if (frames <= 0 || n_lists <= 0) return 0;
-  const int per = 2 * ((2 * g.m + g.nominal + 1) | 1);  // scratch bytes per thread
-  const int room = device_smem_optin() - 1024;
+  const int per = 2 * ((g.m + g.nominal) | 1);  // scratch bytes per thread
+  const int fixed = 8 * (g.m + 1);                // reciprocal table
+  const int room = device_smem_optin() - 1024 - fixed;
   if (per > room) return static_cast<int>(cudaErrorInvalidConfiguration);
-  const int tpb = std::max(1, std::min(64, room / per));
+  // 128 lists per CTA where they fit (about 1.3 KB each for M = 504)
+  const int tpb = std::max(1, std::min(128, room / per));
+  const int bytes = fixed + tpb * per;
   cudaError_t err = cudaFuncSetAttribute(reinterpret_cast<const void*>(gen_groups_kernel),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, tpb * per);
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (err != cudaSuccess) return static_cast<int>(err);
   const int64_t items = frames * n_lists;
-  gen_groups_kernel<<<static_cast<unsigned>((items + tpb - 1) / tpb), tpb, tpb * per,
+  gen_groups_kernel<<<static_cast<unsigned>((items + tpb - 1) / tpb), tpb, bytes,
                       static_cast<cudaStream_t>(stream)>>>(g.m, g.G, g.balanced, g.nominal, g.k_overlap,
                                                            g.schedule_seed, frame0, frames, list0, n_lists,
                                                            g.list_slots, out);
