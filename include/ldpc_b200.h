@@ -143,6 +143,22 @@ int ldpcb_decode_host(ldpcb_code code, ldpcb_schedule s, int64_t frames, const f
 int ldpcb_simulate_device(ldpcb_code code, ldpcb_schedule s, double sigma2, uint64_t channel_seed,
                           int64_t frame_begin, int64_t frames, int max_iters, int early_stop, int64_t *d_counters,
                           void *stream);
+/* ldpcb_simulate_device with per-frame outcomes (any output may be NULL):
+ * bit_errors[f] = hard-decision weight, iterations[f], converged[f] */
+int ldpcb_simulate_frames_device(ldpcb_code code, ldpcb_schedule s, double sigma2, uint64_t channel_seed,
+                                 int64_t frame_begin, int64_t frames, int max_iters, int early_stop,
+                                 int32_t *d_bit_errors, int32_t *d_iterations, uint8_t *d_converged,
+                                 int64_t *d_counters, void *stream);
+/* run_sweep (sim.hpp:96-186) on one GPU: per Eb/N0 point, frames 0,1,...
+ * in waves (wave_frames = 0: automatic) until the smallest prefix holding
+ * min_frame_errors frame errors, or max_frames. out: 11 doubles per point =
+ * frames, bit_errors, frame_errors, converged_frames, ber, fer,
+ * mean_iters_converged, mean_iters_all, iter_limit, wall_seconds, ebn0_db
+ * (SimResult, sim.hpp:44-56). Use a per-frame schedule for the harness's
+ * own grouping. Rate = (n - m) / n as in run_sweep. */
+int ldpcb_run_sweep_host(ldpcb_code code, ldpcb_schedule s, const double *ebn0_db, int n_points, int iter_limit,
+                         int64_t max_frames, int min_frame_errors, uint64_t channel_seed, int64_t wave_frames,
+                         double *out);
 /* ldpcb_simulate_device with host counters; blocks until done */
 int ldpcb_simulate_host(ldpcb_code code, ldpcb_schedule s, double sigma2, uint64_t channel_seed, int64_t frame_begin,
                         int64_t frames, int max_iters, int early_stop, int64_t *counters);

@@ -28,7 +28,9 @@ from .api import (  # noqa: F401
     set_lazy_totals,
     set_tuning,
     sigma2_from_ebn0,
+    run_sweep_native,
     simulate,
+    simulate_frames,
     transmit_all_zero,
 )
 from . import configs  # noqa: F401

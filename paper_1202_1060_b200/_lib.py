@@ -48,6 +48,8 @@ _SIGS = {
     "ldpcb_schedule_disjoint": (C.c_int, [vp, C.c_int, u64, C.POINTER(vp)]),
     "ldpcb_schedule_nondisjoint": (C.c_int, [vp, C.c_int, dbl, u64, C.POINTER(vp)]),
     "ldpcb_schedule_windows": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
+    "ldpcb_simulate_frames_device": (C.c_int, [vp, vp, dbl, u64, i64, i64, C.c_int, C.c_int, vp, vp, vp, vp, vp]),
+    "ldpcb_run_sweep_host": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, i64, C.c_int, u64, i64, vp]),
     "ldpcb_schedule_per_frame": (C.c_int, [vp, C.c_int, C.c_int, dbl, u64, C.c_int, C.POINTER(vp)]),
     "ldpcb_schedule_per_frame_groups_device": (C.c_int, [vp, vp, i64, i64, C.c_int, vp, vp]),
     "ldpcb_schedule_dims": (C.c_int, [vp, P32, P32, P32, P32, PD, P64, P64]),

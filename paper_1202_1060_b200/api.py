@@ -454,6 +454,38 @@ def simulate(g, s, sigma2: float, channel_seed: int, frame_begin: int, frames: i
     return counters
 
 
+def simulate_frames(g, s, sigma2: float, channel_seed: int, frame_begin: int, frames: int, max_iters: int,
+                    early_stop: bool = True, stream=None):
+    """Per-frame outcomes of frames [frame_begin, frame_begin+frames) (run_frame,
+    sim.hpp:111-124): device int32 bit_errors, int32 iterations, uint8 converged."""
+    torch = _torch()
+    be = torch.empty(frames, dtype=torch.int32, device="cuda")
+    it = torch.empty(frames, dtype=torch.int32, device="cuda")
+    cv = torch.empty(frames, dtype=torch.uint8, device="cuda")
+    check(
+        lib.ldpcb_simulate_frames_device(
+            g.handle, s.handle, sigma2, channel_seed, frame_begin, frames, max_iters, int(early_stop), _vp(be),
+            _vp(it), _vp(cv), None, _stream(stream),
+        ),
+        "simulate_frames",
+    )
+    return be, it, cv
+
+
+def run_sweep_native(g, s, ebn0_db, iter_limit: int, max_frames: int, min_frame_errors: int, channel_seed: int = 1,
+                     wave_frames: int = 0) -> list[dict]:
+    """run_sweep (sim.hpp:96-186) on the current GPU through ldpcb_run_sweep_host:
+    one SimResult dict per Eb/N0 point."""
+    pts = np.ascontiguousarray(list(ebn0_db), np.float64)
+    out = np.zeros((len(pts), 11), np.float64)
+    check(lib.ldpcb_run_sweep_host(g.handle, s.handle, _vp(pts), len(pts), iter_limit, max_frames, min_frame_errors,
+                                   channel_seed, wave_frames, _vp(out)), "run_sweep")
+    keys = ("frames", "bit_errors", "frame_errors", "converged_frames", "ber", "fer", "mean_iters_converged",
+            "mean_iters_all", "iter_limit", "wall_seconds", "ebn0_db")
+    ints = {"frames", "bit_errors", "frame_errors", "converged_frames", "iter_limit"}
+    return [{k: (int(v) if k in ints else float(v)) for k, v in zip(keys, row)} for row in out]
+
+
 @dataclass
 class DecodeOutcome:
     """decoder.hpp:31-37."""

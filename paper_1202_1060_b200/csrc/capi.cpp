@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <chrono>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -610,36 +611,149 @@ int ldpcb_decode_host(ldpcb_code code, ldpcb_schedule s, int64_t frames, const f
   });
 }
 
+namespace {
+// Channel + decode of frames [frame_begin, frame_begin+frames) in chunks
+// (sim.hpp:111-124); optional per-frame outcomes and accumulated counters.
+void simulate_frames(ldpcb_code code, ldpcb_schedule s, double sigma2, uint64_t channel_seed, int64_t frame_begin,
+                     int64_t frames, int max_iters, int early_stop, int32_t* d_bit_errors, int32_t* d_iterations,
+                     uint8_t* d_converged, int64_t* d_counters, void* stream) {
+  check_pair(code, s);
+  need(max_iters >= 1, "max_iters must be >= 1");
+  need(frames >= 0 && frame_begin >= 0, "bad frame range");
+  need(sigma2 > 0.0, "sigma2 must be positive");
+  if (frames == 0) return;
+  const auto g = dev_graph(code, s);
+  const ldpcb::Plan p0 = ldpcb::plan_decode(g, frames);
+  if (p0.kernel == 0) throw std::runtime_error("no decoder plan for this code (check degree or memory)");
+  auto st = static_cast<cudaStream_t>(stream);
+  int64_t chunk = std::max<int64_t>(p0.fpc, (int64_t{256} << 20) / (4 * g.n));
+  chunk = std::min<int64_t>(chunk, frames);
+  float* scratch = nullptr;
+  cuda_check(cudaMallocAsync(&scratch, chunk * g.n * sizeof(float), st), "cudaMallocAsync");
+  for (int64_t c0 = 0; c0 < frames; c0 += chunk) {
+    const int64_t cnt = std::min(chunk, frames - c0);
+    launch(ldpcb::launch_channel(g.n, sigma2, channel_seed, frame_begin + c0, cnt, scratch, stream), "channel");
+    ldpcb::DecodeArgs a;
+    a.frame0 = frame_begin + c0;
+    a.frames = cnt;
+    a.llr = scratch;
+    a.max_iters = max_iters;
+    a.early_stop = early_stop != 0;
+    a.counters = reinterpret_cast<unsigned long long*>(d_counters);
+    if (d_bit_errors) a.bit_errors = d_bit_errors + c0;
+    if (d_iterations) a.iterations = d_iterations + c0;
+    if (d_converged) a.converged = d_converged + c0;
+    launch(ldpcb::launch_decode(g, a, stream, nullptr), "decode kernel");
+  }
+  cuda_check(cudaFreeAsync(scratch, st), "cudaFreeAsync");
+}
+}  // namespace
+
 int ldpcb_simulate_device(ldpcb_code code, ldpcb_schedule s, double sigma2, uint64_t channel_seed, int64_t frame_begin,
                           int64_t frames, int max_iters, int early_stop, int64_t* d_counters, void* stream) {
   return guard([&] {
-    check_pair(code, s);
-    need(max_iters >= 1, "max_iters must be >= 1");
-    need(frames >= 0 && frame_begin >= 0, "bad frame range");
-    need(sigma2 > 0.0, "sigma2 must be positive");
     need(d_counters != nullptr, "null counters");
-    if (frames == 0) return LDPCB_OK;
-    const auto g = dev_graph(code, s);
-    const ldpcb::Plan p0 = ldpcb::plan_decode(g, frames);
-    if (p0.kernel == 0) throw std::runtime_error("no decoder plan for this code (check degree or memory)");
-    auto st = static_cast<cudaStream_t>(stream);
-    int64_t chunk = std::max<int64_t>(p0.fpc, (int64_t{256} << 20) / (4 * g.n));
-    chunk = std::min<int64_t>(chunk, frames);
-    float* scratch = nullptr;
-    cuda_check(cudaMallocAsync(&scratch, chunk * g.n * sizeof(float), st), "cudaMallocAsync");
-    for (int64_t c0 = 0; c0 < frames; c0 += chunk) {
-      const int64_t cnt = std::min(chunk, frames - c0);
-      launch(ldpcb::launch_channel(g.n, sigma2, channel_seed, frame_begin + c0, cnt, scratch, stream), "channel");
-      ldpcb::DecodeArgs a;
-      a.frame0 = frame_begin + c0;
-      a.frames = cnt;
-      a.llr = scratch;
-      a.max_iters = max_iters;
-      a.early_stop = early_stop != 0;
-      a.counters = reinterpret_cast<unsigned long long*>(d_counters);
-      launch(ldpcb::launch_decode(g, a, stream, nullptr), "decode kernel");
+    simulate_frames(code, s, sigma2, channel_seed, frame_begin, frames, max_iters, early_stop, nullptr, nullptr,
+                    nullptr, d_counters, stream);
+    return LDPCB_OK;
+  });
+}
+
+int ldpcb_simulate_frames_device(ldpcb_code code, ldpcb_schedule s, double sigma2, uint64_t channel_seed,
+                                 int64_t frame_begin, int64_t frames, int max_iters, int early_stop,
+                                 int32_t* d_bit_errors, int32_t* d_iterations, uint8_t* d_converged,
+                                 int64_t* d_counters, void* stream) {
+  return guard([&] {
+    need(d_bit_errors || d_iterations || d_converged || d_counters, "no outputs");
+    simulate_frames(code, s, sigma2, channel_seed, frame_begin, frames, max_iters, early_stop, d_bit_errors,
+                    d_iterations, d_converged, d_counters, stream);
+    return LDPCB_OK;
+  });
+}
+
+// run_sweep (sim.hpp:96-186) on the device: waves of frames, per-frame
+// outcomes copied back, and the point stops at the smallest frame index whose
+// prefix holds min_frame_errors frame errors (or at max_frames). The result
+// does not depend on the wave size, as in the reference.
+int ldpcb_run_sweep_host(ldpcb_code code, ldpcb_schedule s, const double* ebn0_db, int n_points, int iter_limit,
+                         int64_t max_frames, int min_frame_errors, uint64_t channel_seed, int64_t wave_frames,
+                         double* out) {
+  return guard([&] {
+    check_pair(code, s);
+    need(ebn0_db != nullptr && n_points >= 1, "need at least one Eb/N0 point");
+    need(min_frame_errors >= 1, "min_frame_errors must be >= 1");
+    need(max_frames >= 1, "max_frames must be >= 1");
+    need(iter_limit >= 1, "max_iters must be >= 1");
+    need(out != nullptr, "null output");
+    const auto& h = code->impl->host;
+    const double rate = static_cast<double>(h.n - h.m) / h.n;
+    int64_t cap = wave_frames > 0 ? wave_frames : (int64_t{1} << 20);
+    cap = std::min(cap, max_frames);
+    cudaStream_t st;
+    cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+    int32_t *d_be = nullptr, *d_it = nullptr;
+    uint8_t* d_cv = nullptr;
+    std::vector<int32_t> be(cap), it(cap);
+    std::vector<uint8_t> cv(cap);
+    auto cleanup = [&] {
+      if (d_be) cudaFreeAsync(d_be, st);
+      if (d_it) cudaFreeAsync(d_it, st);
+      if (d_cv) cudaFreeAsync(d_cv, st);
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    };
+    try {
+      cuda_check(cudaMallocAsync(&d_be, cap * 4, st), "cudaMallocAsync");
+      cuda_check(cudaMallocAsync(&d_it, cap * 4, st), "cudaMallocAsync");
+      cuda_check(cudaMallocAsync(&d_cv, cap, st), "cudaMallocAsync");
+      for (int pt = 0; pt < n_points; ++pt) {
+        const auto t0 = std::chrono::steady_clock::now();
+        const double sigma2 = ldpcb::awgn_sigma2(ebn0_db[pt], rate);
+        int64_t produced = 0, stop = -1, fe_total = 0, conv = 0;
+        long long bit_errors = 0, iter_sum = 0, iter_conv = 0;
+        // the first wave is small so that high-FER points stop early
+        int64_t wave = std::min<int64_t>(cap, 4096);
+        while (stop < 0) {
+          const int64_t cnt = std::min(wave, max_frames - produced);
+          simulate_frames(code, s, sigma2, channel_seed, produced, cnt, iter_limit, 1, d_be, d_it, d_cv, nullptr, st);
+          cuda_check(cudaMemcpyAsync(be.data(), d_be, cnt * 4, cudaMemcpyDeviceToHost, st), "D2H");
+          cuda_check(cudaMemcpyAsync(it.data(), d_it, cnt * 4, cudaMemcpyDeviceToHost, st), "D2H");
+          cuda_check(cudaMemcpyAsync(cv.data(), d_cv, cnt, cudaMemcpyDeviceToHost, st), "D2H");
+          cuda_check(cudaStreamSynchronize(st), "sync");
+          for (int64_t i = 0; i < cnt; ++i) {  // prefix scan (sim.hpp:150-158) + aggregation (:162-181)
+            bit_errors += be[i];
+            fe_total += be[i] > 0;
+            conv += cv[i];
+            iter_sum += it[i];
+            iter_conv += cv[i] ? it[i] : 0;
+            if (fe_total >= min_frame_errors) {
+              stop = produced + i;
+              break;
+            }
+          }
+          produced += cnt;
+          if (stop < 0 && produced >= max_frames) stop = max_frames - 1;
+          wave = std::min(cap, 2 * wave);
+        }
+        const double frames = static_cast<double>(stop + 1);
+        double* o = out + 11 * pt;
+        o[0] = frames;
+        o[1] = static_cast<double>(bit_errors);
+        o[2] = static_cast<double>(fe_total);
+        o[3] = static_cast<double>(conv);
+        o[4] = static_cast<double>(bit_errors) / (frames * h.n);
+        o[5] = static_cast<double>(fe_total) / frames;
+        o[6] = conv > 0 ? static_cast<double>(iter_conv) / conv : 0.0;
+        o[7] = static_cast<double>(iter_sum) / frames;
+        o[8] = iter_limit;
+        o[9] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        o[10] = ebn0_db[pt];
+      }
+    } catch (...) {
+      cleanup();
+      throw;
     }
-    cuda_check(cudaFreeAsync(scratch, st), "cudaFreeAsync");
+    cleanup();
     return LDPCB_OK;
   });
 }

@@ -404,7 +404,7 @@ finish:
         out[b] = static_cast<uint8_t>(byte);
         errs += __popc(byte);
       }
-    } else if (a.bits || a.counters) {
+    } else if (a.bits || a.counters || a.bit_errors) {
       for (int v = j0; v < n; v += jstep) {
         const int bit = P[v * FPC + i] < 0.f;
         if (a.bits) a.bits[(f0 + f) * n + v] = static_cast<uint8_t>(bit);
@@ -421,6 +421,7 @@ finish:
     if (a.converged) a.converged[f0 + tid] = static_cast<uint8_t>(s_conv[tid]);
   }
   __syncthreads();
+  if (a.bit_errors && tid < nf) a.bit_errors[f0 + tid] = s_berr[tid];
   if (tid == 0 && a.counters) {
     unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
     for (int ff = 0; ff < nf; ++ff) {
@@ -740,6 +741,7 @@ int launch_decode(const DevGraph& g, const DecodeArgs& a_in, void* stream, Plan*
     if (a.bits) b.bits = a.bits + c0 * (a.bits_packed ? nb : n);
     if (a.iterations) b.iterations = a.iterations + c0;
     if (a.converged) b.converged = a.converged + c0;
+    if (a.bit_errors) b.bit_errors = a.bit_errors + c0;
     if (a.posterior) b.posterior = a.posterior + c0 * n;
     if (a.trace) b.trace = a.trace + c0 * a.max_iters;
     if (a.c2v_out) b.c2v_out = a.c2v_out + c0 * g.E;

@@ -48,6 +48,7 @@ struct DecodeArgs {
   int bits_packed = 0;
   int32_t* iterations = nullptr;
   uint8_t* converged = nullptr;
+  int32_t* bit_errors = nullptr;  // per-frame hard-decision weight (all-zero codeword errors)
   float* posterior = nullptr;
   int32_t* trace = nullptr;  // [frames][max_iters]
   unsigned long long* counters = nullptr;  // 6 x int64, accumulated

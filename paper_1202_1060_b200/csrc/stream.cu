@@ -263,6 +263,7 @@ __global__ void stream_final(ChunkState s, const DecodeArgs a, int64_t frame0) {
     const int it = a.early_stop ? s.iters[f] : a.max_iters;
     if (a.iterations) a.iterations[frame0 + f] = it;
     if (a.converged) a.converged[frame0 + f] = static_cast<uint8_t>(s.conv[f]);
+    if (a.bit_errors) a.bit_errors[frame0 + f] = s.berr[f];
     c[0] = 1;
     c[1] = s.berr[f];
     c[2] = s.berr[f] > 0;

@@ -114,6 +114,89 @@ def run_sweep(code, sched, ebn0_db, frames: int, max_iters: int, early_stop: boo
     return [run_point(be, code.n_vars, e, frames, max_iters) for e in ebn0_db]
 
 
+def frames_backend(code, sched, max_iters: int, channel_seed: int = 1):
+    """Per-frame outcomes (bit_errors, iterations, converged) of frames
+    [begin, begin+count) on the current GPU (ldpcb_simulate_frames_device)."""
+    from . import api
+
+    def run(ebn0_db: float, begin: int, count: int):
+        sigma2 = api.sigma2_from_ebn0(ebn0_db, code.rate)
+        return api.simulate_frames(code, sched, sigma2, channel_seed, begin, count, max_iters)
+
+    return run
+
+
+def _gather_wave(outcome, count: int, world: int):
+    """Concatenate every rank's per-frame outcomes in frame order: one
+    all_gather of an int32 [3, ceil(count/world)+1] block per rank (shard
+    sizes differ by at most one frame)."""
+    import torch
+    import torch.distributed as dist
+
+    be, it, cv = outcome
+    width = count // world + 1
+    mine = torch.zeros((3, width), dtype=torch.int32, device=be.device)
+    n = be.numel()
+    mine[0, :n], mine[1, :n], mine[2, :n] = be, it, cv.to(torch.int32)
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine)
+    cols = [parts[r][:, : shard(count, r, world)[1]] for r in range(world)]
+    return torch.cat(cols, dim=1).cpu().numpy()
+
+
+def run_point_prefix(backend: Callable, n_vars: int, ebn0_db: float, max_frames: int, min_frame_errors: int,
+                     iter_limit: int, wave_cap: int = 1 << 20) -> SimResult:
+    """One Eb/N0 point with the reference's stopping rule (sim.hpp:126-160):
+    frames 0,1,... in waves, stop at the smallest frame index whose prefix
+    holds min_frame_errors frame errors, or at max_frames. Each wave is
+    sharded across ranks and the per-frame outcomes are all-gathered in frame
+    order, so the result does not depend on the GPU count or wave size."""
+    import numpy as np
+    import torch.distributed as dist
+
+    if min_frame_errors < 1:
+        raise ValueError("min_frame_errors must be >= 1")
+    if max_frames < 1:
+        raise ValueError("max_frames must be >= 1")
+    world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank() if world > 1 else 0
+    t0 = time.perf_counter()
+    produced, stop, wave = 0, -1, min(4096 * world, wave_cap)
+    c = np.zeros(6, np.int64)
+    fe = 0
+    while stop < 0:
+        cnt = min(wave, max_frames - produced)
+        b, k = shard(cnt, rank, world)
+        out = backend(ebn0_db, produced + b, k)
+        if world > 1:
+            arr = _gather_wave(out, cnt, world)
+        else:
+            arr = np.stack([x.cpu().numpy().astype(np.int64) for x in out])
+        be, it, cv = (np.asarray(x, np.int64) for x in arr)
+        cum = fe + np.cumsum(be > 0)
+        hit = np.flatnonzero(cum >= min_frame_errors)
+        take = int(hit[0]) + 1 if hit.size else cnt
+        be, it, cv = be[:take], it[:take], cv[:take]
+        c += [take, be.sum(), (be > 0).sum(), cv.sum(), it.sum(), (it * cv).sum()]
+        fe = int(c[2])
+        produced += cnt
+        if hit.size:
+            stop = produced - cnt + take - 1
+        elif produced >= max_frames:
+            stop = max_frames - 1
+        wave = min(2 * wave, wave_cap)
+    return aggregate(c.tolist(), n_vars, ebn0_db, iter_limit, time.perf_counter() - t0)
+
+
+def run_sweep_prefix(code, sched, ebn0_db, iter_limit: int, max_frames: int, min_frame_errors: int,
+                     channel_seed: int = 1, backend: Callable | None = None) -> list[SimResult]:
+    """run_sweep (sim.hpp:96-186) with its min-frame-errors stopping rule."""
+    if not ebn0_db:
+        raise ValueError("need at least one Eb/N0 point")
+    be = backend or frames_backend(code, sched, iter_limit, channel_seed)
+    return [run_point_prefix(be, code.n_vars, e, max_frames, min_frame_errors, iter_limit) for e in ebn0_db]
+
+
 def clopper_pearson(k: int, n: int, alpha: float = 0.05) -> tuple[float, float]:
     """Exact binomial confidence interval (FER)."""
     from scipy.stats import beta
