@@ -207,6 +207,17 @@ inline GroupSchedule make_nondisjoint_schedule(const TannerGraph& g, int n_group
   return GroupSchedule::from_handle(h);
 }
 
+// run_sweep's grouping (sim.hpp:113-117): each frame draws its own groups
+// from mix_seed(schedule_seed, frame_id), redrawn every iteration when
+// regroup_each_iteration (decoder.hpp:153-156); generated on the device.
+inline GroupSchedule make_per_frame_schedule(const TannerGraph& g, ScheduleKind kind, int n_groups, double overlap,
+                                             std::uint64_t schedule_seed, bool regroup_each_iteration = true) {
+  ldpcb_schedule h = nullptr;
+  detail::check(ldpcb_schedule_per_frame(g.handle(), static_cast<int>(kind), n_groups, overlap, schedule_seed,
+                                         regroup_each_iteration ? 1 : 0, &h));
+  return GroupSchedule::from_handle(h);
+}
+
 inline GroupSchedule make_window_schedule(const TannerGraph& g, int n_groups, int window, int stride) {
   ldpcb_schedule h = nullptr;
   const int kind = window > stride ? LDPCB_NONDISJOINT : LDPCB_DISJOINT;
@@ -305,6 +316,49 @@ inline std::array<int64_t, 6> simulate(const TannerGraph& g, const GroupSchedule
   detail::check(ldpcb_simulate_host(g.handle(), s.handle(), sigma2_from_ebn0(ebn0_db, rate), channel_seed,
                                     frame_begin, frames, max_iters, early_stop ? 1 : 0, c.data()));
   return c;
+}
+
+// SimResult (sim.hpp:44-56)
+struct SimResult {
+  double ebn0_db = 0.0;
+  long frames = 0;
+  long long bit_errors = 0;
+  long frame_errors = 0;
+  long converged_frames = 0;
+  double ber = 0.0;
+  double fer = 0.0;
+  double mean_iters_converged = 0.0;
+  double mean_iters_all = 0.0;
+  int iter_limit = 0;
+  double wall_seconds = 0.0;
+};
+
+// run_sweep (sim.hpp:96-186) on the calling thread's GPU: frames 0,1,... per
+// point until the smallest prefix holding min_frame_errors frame errors, or
+// max_frames. Pass make_per_frame_schedule for the harness's own grouping.
+inline std::vector<SimResult> run_sweep(const TannerGraph& g, const GroupSchedule& s,
+                                        const std::vector<double>& ebn0_db, int iter_limit, long max_frames,
+                                        int min_frame_errors, std::uint64_t channel_seed = 1) {
+  std::vector<double> raw(11 * ebn0_db.size());
+  detail::check(ldpcb_run_sweep_host(g.handle(), s.handle(), ebn0_db.data(), static_cast<int>(ebn0_db.size()),
+                                     iter_limit, max_frames, min_frame_errors, channel_seed, 0, raw.data()));
+  std::vector<SimResult> out(ebn0_db.size());
+  for (std::size_t i = 0; i < out.size(); ++i) {
+    const double* o = raw.data() + 11 * i;
+    auto& r = out[i];
+    r.frames = static_cast<long>(o[0]);
+    r.bit_errors = static_cast<long long>(o[1]);
+    r.frame_errors = static_cast<long>(o[2]);
+    r.converged_frames = static_cast<long>(o[3]);
+    r.ber = o[4];
+    r.fer = o[5];
+    r.mean_iters_converged = o[6];
+    r.mean_iters_all = o[7];
+    r.iter_limit = static_cast<int>(o[8]);
+    r.wall_seconds = o[9];
+    r.ebn0_db = o[10];
+  }
+  return out;
 }
 
 }  // namespace ldpc_b200

@@ -127,6 +127,18 @@ static void gpu_cases() {
   CHECK(sim[0] == 1000 && sim[2] <= sim[0] && sim[4] >= sim[0]);
   std::printf("simulate 1000 frames @2.0 dB: frame errors %lld, mean iterations %.3f\n",
               static_cast<long long>(sim[2]), static_cast<double>(sim[4]) / sim[0]);
+
+  // run_sweep with the harness's per-frame regrouping (sim.hpp:96-186)
+  const GroupSchedule pf = make_per_frame_schedule(c1, ScheduleKind::nondisjoint, 8, 0.25, 2, true);
+  const auto res = run_sweep(c1, pf, {1.5, 2.0}, 20, 100000, 25);
+  CHECK(res.size() == 2 && res[0].ebn0_db == 1.5 && res[1].ebn0_db == 2.0);
+  for (const auto& r : res) {
+    CHECK(r.frame_errors == 25 && r.frames < 100000 && r.iter_limit == 20);
+    CHECK(r.fer == static_cast<double>(r.frame_errors) / r.frames);
+  }
+  CHECK(res[1].frames > res[0].frames);
+  CHECK_THROWS_AS(run_sweep(c1, pf, {}, 20, 10, 1), std::invalid_argument);
+  CHECK_THROWS_AS(make_per_frame_schedule(c1, ScheduleKind::nondisjoint, 8, 0.9, 2), std::invalid_argument);
 }
 
 int main(int argc, char** argv) {
