@@ -103,7 +103,7 @@ struct SchedImpl {
   ldpcb::KernelTables tables;
   std::mutex mu;
   struct Dev {
-    int32_t *cn_off, *cn_rec, *fix_off, *fix_rec, *all_vn_rec, *all_rec, *edge_slot;
+    int32_t *cn_off, *cn_rec, *fix_off, *fix_rec, *all_vn_rec, *tot_vn_rec, *all_rec, *edge_slot;
     std::vector<void*> ptrs;
   };
   std::map<int, Dev> dev;
@@ -123,9 +123,10 @@ struct SchedImpl {
     x.fix_off = upload(tables.fix_off);
     x.fix_rec = upload(tables.fix_rec);
     x.all_vn_rec = upload(tables.all_vn_rec);
+    x.tot_vn_rec = upload(tables.tot_vn_rec);
     x.all_rec = upload(tables.all_rec);
     x.edge_slot = upload(tables.edge_slot);
-    x.ptrs = {x.cn_off, x.cn_rec, x.fix_off, x.fix_rec, x.all_vn_rec, x.all_rec, x.edge_slot};
+    x.ptrs = {x.cn_off, x.cn_rec, x.fix_off, x.fix_rec, x.all_vn_rec, x.tot_vn_rec, x.all_rec, x.edge_slot};
     return dev.emplace(d, std::move(x)).first->second;
   }
 };
@@ -216,6 +217,7 @@ ldpcb::DevGraph dev_graph(ldpcb_code code, ldpcb_schedule s) {
   g.fix_off = d.fix_off;
   g.fix_rec = d.fix_rec;
   g.all_vn_rec = d.all_vn_rec;
+  g.tot_vn_rec = d.tot_vn_rec;
   g.all_rec = d.all_rec;
   const auto& sh = s->impl->host;
   g.per_frame = sh.per_frame;

@@ -85,6 +85,16 @@ __device__ __forceinline__ void sts(float* p, const FVec<FV>& x) {
   }
 }
 
+// Keeps the consumers of a prefetched value below this point: the compiler
+// otherwise hoists address arithmetic on a record loaded one phase ahead up
+// to the load and stalls on it.
+__device__ __forceinline__ void pin(int4& t) { asm volatile("" : "+r"(t.x), "+r"(t.y), "+r"(t.z), "+r"(t.w)); }
+template <int N>
+__device__ __forceinline__ void pin(int (&r)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) asm volatile("" : "+r"(r[i]));
+}
+
 // live: bit i set when frame i of this thread's vector is still decoding
 template <int D, bool EXACT, int FPC, int FV, bool ALL_LIVE>
 __device__ __forceinline__ void cn_update(float* __restrict__ c2v, float* __restrict__ P,
@@ -180,6 +190,16 @@ __device__ __forceinline__ unsigned parity(const float* __restrict__ P, const in
 
 constexpr int max_threads_for(int D, int FV) { return FV == 2 ? 256 : (D <= 8 ? 512 : (D <= 16 ? 256 : 128)); }
 
+#ifdef LDPCB_PHASE_TIMING
+// Debug build only (scripts/phase_timing.py): CTA-level cycle counts of the
+// phases of decode_resident, taken by thread 0 between barriers: [CN phase,
+// fix-up phase, iteration end, whole kernel, group phases, CTAs].
+__device__ unsigned long long g_phase_cycles[8];
+#define PT_MARK(var) long long var = clock64()
+#else
+#define PT_MARK(var)
+#endif
+
 // RND: per-frame random grouping (host.hpp ScheduleData::per_frame). Each
 // frame's ordered CN groups come from a generated list (gen_groups_kernel);
 // the CN records are the per-CN ones (no in-place posterior updates) and
@@ -205,11 +225,12 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
   int* const s_iters = s_weight + FPC;
   int* const s_conv = s_iters + FPC;
   int* const s_berr = s_conv + FPC;
-  int* const s_cn_off = s_berr + FPC;         // [G+1] staged group tables
-  int* const s_fix_off = s_cn_off + g.G + 1;  // [G+1]
-  uint16_t* const s_list = reinterpret_cast<uint16_t*>(s_fix_off + g.G + 1);  // RND: [FPC][slots]
+  // staged group tables: s_go[g] = {first CN item, end, first fix-up item, end}
+  int4* const s_go = reinterpret_cast<int4*>((reinterpret_cast<uintptr_t>(s_berr + FPC) + 15) & ~uintptr_t{15});
+  uint16_t* const s_list = reinterpret_cast<uint16_t*>(s_go + g.G);  // RND: [FPC][slots]
   const int slots = a.list_slots;
-  const int4* const all_vn = reinterpret_cast<const int4*>(g.all_vn_rec);
+  const int4* const all_vn = reinterpret_cast<const int4*>(g.all_vn_rec);  // indexed by VN (RND)
+  const int4* const tot_vn = reinterpret_cast<const int4*>(g.tot_vn_rec);  // bank-coloured order
   const int4* const fix_vn = reinterpret_cast<const int4*>(g.fix_rec);
 
   const int64_t f0 = static_cast<int64_t>(blockIdx.x) * FPC;
@@ -241,9 +262,8 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
     s_conv[tid] = 0;
     s_berr[tid] = 0;
   }
-  for (int i = tid; i <= g.G; i += nt) {
-    s_cn_off[i] = __ldg(g.cn_off + i);
-    s_fix_off[i] = __ldg(g.fix_off + i);
+  for (int i = tid; i < g.G; i += nt) {
+    s_go[i] = make_int4(__ldg(g.cn_off + i), __ldg(g.cn_off + i + 1), __ldg(g.fix_off + i), __ldg(g.fix_off + i + 1));
   }
   if (a.trace)
     for (int i = tid; i < nf * a.max_iters; i += nt) a.trace[f0 * a.max_iters + i] = -1;
@@ -258,10 +278,17 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
   // records are prefetched one phase ahead: the first CN item of the next
   // group and the first fix-up item of the current one
   CnRecord<D, EXACT> next_cn;
-  if (!RND && j0 < s_cn_off[1] - s_cn_off[0]) next_cn.load(g.cn_rec + static_cast<size_t>(s_cn_off[0] + j0) * CS);
+  if (!RND && j0 < s_go[0].y - s_go[0].x) next_cn.load(g.cn_rec + static_cast<size_t>(s_go[0].x + j0) * CS);
+  // the current group's offsets, in registers; the next group's are read one
+  // group ahead so no shared-memory read sits on the critical path
+  int4 go = s_go[0];
 
   const bool dump = a.max_subiters > 0;
   int sub = 0;
+#ifdef LDPCB_PHASE_TIMING
+  unsigned long long pt_cn = 0, pt_fix = 0, pt_end = 0, pt_groups = 0;
+  const long long pt_start = clock64();
+#endif
   for (int iter = 1; iter <= a.max_iters; ++iter) {
     if constexpr (RND) {
       if (iter == 1 || a.n_lists > 1) {  // this iteration's groups (decoder.hpp:153-156)
@@ -277,8 +304,8 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
       if (dump && sub == a.max_subiters) goto finish;
       ++sub;
       // CN phase: every (CN of the group, frame vector); Jacobi within the group
-      const int c0 = s_cn_off[grp], cn = s_cn_off[grp + 1] - c0;
       if constexpr (RND) {
+        const int c0 = s_go[grp].x, cn = s_go[grp].y - c0;
         const uint16_t* lst = s_list + fb * slots + c0;
         if (live)
           for (int j = j0; j < cn; j += jstep)
@@ -294,7 +321,10 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
         __syncthreads();
         continue;
       }
-      const int x0 = s_fix_off[grp], xn = s_fix_off[grp + 1] - x0;
+      PT_MARK(pt_a);
+      const int c0 = go.x, cn = go.y - go.x;
+      const int x0 = go.z, xn = go.w - go.z;
+      const int4 ngo = s_go[grp + 1 < g.G ? grp + 1 : 0];  // one broadcast read, one group ahead
       int4 fix_first = make_int4(0, 0, 0, 0);
       if (j0 < xn) fix_first = __ldg(fix_vn + static_cast<size_t>(x0 + j0) * vs4);
       if (live && j0 < cn) {
@@ -309,12 +339,10 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
             cn_update<D, EXACT, FPC, FV, false>(c2v, P, CnRecord<D, EXACT>(rec + j * CS), live);
         }
       }
-      {
-        const int ng = grp + 1 < g.G ? grp + 1 : 0;
-        if (j0 < s_cn_off[ng + 1] - s_cn_off[ng])
-          next_cn.load(g.cn_rec + static_cast<size_t>(s_cn_off[ng] + j0) * CS);
-      }
+      if (j0 < ngo.y - ngo.x) next_cn.load(g.cn_rec + static_cast<size_t>(ngo.x + j0) * CS);
       __syncthreads();
+      PT_MARK(pt_b);
+      pin(fix_first);
       // VNs shared by two or more CNs of the group: exact re-sum (a stopped
       // frame re-sums to the value it already holds)
       if (xn > 0) {
@@ -325,13 +353,22 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
         }
         __syncthreads();
       }
+      pin(next_cn.r);
+      go = ngo;
+#ifdef LDPCB_PHASE_TIMING
+      const long long pt_c = clock64();
+      pt_cn += pt_b - pt_a;
+      pt_fix += pt_c - pt_b;
+      ++pt_groups;
+#endif
     }
     if (dump) continue;
+    PT_MARK(pt_d);
     const bool check = a.early_stop || a.trace || iter == a.max_iters;
     // ---- exact totals (decoder.hpp:162-165): removes the rounding of the
     // in-place posterior updates before hard decisions are taken
     if (!RND && g.recompute && (check || !a.lazy_totals)) {
-      if (live) vn_sum_range<FPC, FV, VS>(c2v, P, L, all_vn, vs4, j0, n, jstep);
+      if (live) vn_sum_range<FPC, FV, VS>(c2v, P, L, tot_vn, vs4, j0, n, jstep);
       __syncthreads();
     }
     if (!check) continue;
@@ -365,13 +402,26 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
       s_active = active;
     }
     __syncthreads();
+#ifdef LDPCB_PHASE_TIMING
+    pt_end += clock64() - pt_d;
+#endif
     live = live_bits(fb);
     if (s_active == 0) break;
   }
+#ifdef LDPCB_PHASE_TIMING
+  if (tid == 0) {
+    atomicAdd(&g_phase_cycles[0], pt_cn);
+    atomicAdd(&g_phase_cycles[1], pt_fix);
+    atomicAdd(&g_phase_cycles[2], pt_end);
+    atomicAdd(&g_phase_cycles[3], static_cast<unsigned long long>(clock64() - pt_start));
+    atomicAdd(&g_phase_cycles[4], pt_groups);
+    atomicAdd(&g_phase_cycles[5], 1ull);
+  }
+#endif
 finish:
   __syncthreads();
   if (dump) {
-    if (!RND && g.recompute) vn_sum_range<FPC, FV, VS>(c2v, P, L, all_vn, vs4, j0, n, jstep);
+    if (!RND && g.recompute) vn_sum_range<FPC, FV, VS>(c2v, P, L, tot_vn, vs4, j0, n, jstep);
     __syncthreads();
     const int E = g.E;
 #pragma unroll
@@ -662,7 +712,7 @@ Plan plan_resident(const DevGraph& g, int64_t frames) {
   const size_t limit = static_cast<size_t>(device_smem_optin()) - 1024;
   const size_t per = frame_bytes(g);
   const size_t list_bytes = g.per_frame ? 2ull * g.list_slots : 0;  // per frame
-  auto bytes = [&](int f) { return f * (per + list_bytes) + 20 * f + 8 * (g.G + 1) + 16; };
+  auto bytes = [&](int f) { return f * (per + list_bytes) + 20 * f + 16 * g.G + 32; };
   int fpc = g_tune_fpc.load();
   if (fpc <= 0) {
     // largest FPC that still lets four CTAs share an SM (their barriers and
@@ -756,6 +806,17 @@ int launch_decode(const DevGraph& g, const DecodeArgs& a_in, void* stream, Plan*
   cudaFreeAsync(lists, st);
   return static_cast<int>(err);
 }
+
+#ifdef LDPCB_PHASE_TIMING
+extern "C" int ldpcb_debug_phase_cycles(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_phase_cycles, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {};
+    cudaMemcpyToSymbol(g_phase_cycles, z, sizeof z);
+  }
+  return static_cast<int>(cudaDeviceSynchronize());
+}
+#endif
 
 int launch_channel(int n, double sigma2, uint64_t seed, int64_t frame0, int64_t frames, float* llr, void* stream) {
   if (frames <= 0) return 0;

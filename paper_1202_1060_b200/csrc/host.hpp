@@ -111,7 +111,8 @@ struct KernelTables {
   bool recompute = false;  // some CN updates a posterior in place
   std::vector<int32_t> cn_off, cn_rec;    // per group
   std::vector<int32_t> fix_off, fix_rec;  // per group: VNs shared by >= 2 CNs
-  std::vector<int32_t> all_vn_rec;        // every VN (exact totals, decoder.hpp:162-165)
+  std::vector<int32_t> all_vn_rec;        // every VN, record v = VN v (decoder.hpp:162-165)
+  std::vector<int32_t> tot_vn_rec;        // the same records in bank-coloured order (exact totals)
   std::vector<int32_t> all_rec;           // every CN in index order (syndrome)
   std::vector<int32_t> edge_slot;         // CN-major edge id -> slot
   int max_cn_items = 0, max_fix_items = 0;

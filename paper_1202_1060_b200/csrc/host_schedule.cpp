@@ -1,6 +1,8 @@
 // host_schedule.cpp -- CN-group schedules and their derived tables.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstdio>
 
 #include "host.hpp"
 #include "rng.cuh"
@@ -163,6 +165,191 @@ int iteration_budget(const ScheduleData& s, int n_checks, int i_max) {
   return static_cast<int>(std::floor(static_cast<double>(n_checks) * i_max / (n_checks + extra)));
 }
 
+namespace {
+
+// Shared-memory bank colouring. A warp of the resident kernel (two frames
+// per CTA) works on 16 consecutive items of a list per half-warp, and each
+// instruction gathers or scatters one 64-bit frame-interleaved element per
+// item: elements whose index is equal mod 16 fall in the same banks and
+// serialise. The annealers below reorder what is free to reorder so that,
+// per (16-item block, column), few items share a colour:
+//  * the edges of each CN (boxplus is symmetric): columns are the record
+//    positions, colour = VN mod 16, for the gathers of P and, separately, the
+//    in-place stores of single-touch posteriors;
+//  * the items of VN-record lists (fix-ups, exact totals): columns are L/P of
+//    the VN and each c2v slot, colour = slot mod 16.
+// Cost = sum over cells of the largest colour count (duplicates counted, a
+// slight overestimate). Deterministic (fixed seeds, fixed move counts).
+constexpr int kBankBlock = 16, kColours = 16;
+
+struct ColourCells {
+  int cols;
+  std::vector<uint8_t> cnt;  // [cell][colour]
+  std::vector<int> best;     // [cell]
+  ColourCells(int cells, int cols_) : cols(cols_), cnt(static_cast<size_t>(cells) * kColours, 0), best(cells, 0) {}
+  int max_of(int cell) const {
+    int m = 0;
+    for (int k = 0; k < kColours; ++k) m = std::max<int>(m, cnt[cell * kColours + k]);
+    return m;
+  }
+};
+
+// perm[off + p] = original edge index (relative to the row) at record position p
+std::vector<int> bank_orders(const CodeData& c, const std::vector<std::vector<int>>& group_cns,
+                             const std::vector<std::vector<char>>& single) {
+  std::vector<int> perm(c.E);
+  for (int r = 0; r < c.m; ++r)
+    for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e) perm[e] = e - c.row_off[r];
+  if (c.n > 32768 || c.m < 2) return perm;
+  const int D = c.max_cdeg;
+  // (group, block) of every CN occurrence
+  struct Occ {
+    int cell0;  // first cell of its block: cells [cell0, cell0 + 2D) = D gather + D store columns
+    int group;
+  };
+  std::vector<std::vector<Occ>> occ(c.m);
+  int nblocks = 0;
+  for (int g = 0; g < static_cast<int>(group_cns.size()); ++g)
+    for (int j = 0; j < static_cast<int>(group_cns[g].size()); ++j) {
+      if (j % kBankBlock == 0) ++nblocks;
+      occ[group_cns[g][j]].push_back({(nblocks - 1) * 2 * D, g});
+    }
+  ColourCells cc(nblocks * 2 * D, 2 * D);
+  auto vn_at = [&](int r, int p) { return c.cols[c.row_off[r] + perm[c.row_off[r] + p]]; };
+  auto add = [&](int r, int p, int sign) {
+    const int v = vn_at(r, p), col = v % kColours;
+    for (const Occ& o : occ[r]) {
+      cc.cnt[(o.cell0 + p) * kColours + col] += sign;
+      if (single[o.group][v]) cc.cnt[(o.cell0 + D + p) * kColours + col] += sign;
+    }
+  };
+  for (int r = 0; r < c.m; ++r)
+    for (int p = 0; p < c.row_off[r + 1] - c.row_off[r]; ++p) add(r, p, +1);
+  long long total = 0;
+  for (int i = 0; i < nblocks * 2 * D; ++i) total += cc.best[i] = cc.max_of(i);
+  const long long c0 = total;
+  const std::vector<int> initial = perm;  // structured codes (QC) may start out conflict-free
+  Stream rng(0x6c64706362616e6bull);
+  static const long long scale = [] {
+    const char* e = std::getenv("LDPCB_BANK_ITERS");  // moves per CN; tuning / A-B only
+    return e ? std::atoll(e) : 1000ll;
+  }();
+  const long long iters = std::min<long long>(8000000, scale * c.m);
+  auto cells_of = [&](int r, int p1, int p2, int* out) {
+    int k = 0;
+    for (const Occ& o : occ[r]) {
+      out[k++] = o.cell0 + p1;
+      out[k++] = o.cell0 + p2;
+      out[k++] = o.cell0 + D + p1;
+      out[k++] = o.cell0 + D + p2;
+    }
+    return k;
+  };
+  int cl[64];
+  for (long long it = 0; it < iters; ++it) {
+    const double T = 2.0 * (1.0 - static_cast<double>(it) / iters) + 0.02;
+    const int r = static_cast<int>(rng.below(c.m));
+    const int deg = c.row_off[r + 1] - c.row_off[r];
+    if (deg < 2 || occ[r].empty() || occ[r].size() > 16) continue;
+    const int p1 = static_cast<int>(rng.below(deg));
+    int p2 = static_cast<int>(rng.below(deg - 1));
+    if (p2 >= p1) ++p2;
+    const int nc = cells_of(r, p1, p2, cl);
+    int old = 0;
+    for (int i = 0; i < nc; ++i) old += cc.best[cl[i]];
+    add(r, p1, -1);
+    add(r, p2, -1);
+    std::swap(perm[c.row_off[r] + p1], perm[c.row_off[r] + p2]);
+    add(r, p1, +1);
+    add(r, p2, +1);
+    int now = 0, fresh[64];
+    for (int i = 0; i < nc; ++i) now += fresh[i] = cc.max_of(cl[i]);
+    const int d = now - old;
+    if (d <= 0 || rng.unit() < std::exp(-d / T)) {
+      for (int i = 0; i < nc; ++i) cc.best[cl[i]] = fresh[i];
+      total += d;
+    } else {
+      add(r, p1, -1);
+      add(r, p2, -1);
+      std::swap(perm[c.row_off[r] + p1], perm[c.row_off[r] + p2]);
+      add(r, p1, +1);
+      add(r, p2, +1);
+    }
+  }
+  if (std::getenv("LDPCB_BANK_DEBUG"))
+    std::fprintf(stderr, "bank_orders: %d cells, cost %.3f -> %.3f per cell (%lld moves)\n", nblocks * 2 * D,
+                 static_cast<double>(c0) / (nblocks * 2 * D), static_cast<double>(total) / (nblocks * 2 * D), iters);
+  return total <= c0 ? perm : initial;
+}
+
+void bank_order_vns(std::vector<int>& vns, int begin, int end, const CodeData& c, const std::vector<int>& edge_slot,
+                    uint64_t seed) {
+  const int count = end - begin;
+  if (count <= kBankBlock || c.n > 32768) return;
+  const int cols = 1 + c.max_vdeg;
+  auto colour = [&](int v, int q) {  // q = 0: L/P of v, else the (q-1)-th c2v slot (-1: none)
+    if (q == 0) return v % kColours;
+    const int j = c.var_off[v] + q - 1;
+    return j < c.var_off[v + 1] ? edge_slot[c.var_edges[j]] % kColours : -1;
+  };
+  const int nblocks = (count + kBankBlock - 1) / kBankBlock;
+  ColourCells cc(nblocks * cols, cols);
+  auto add = [&](int i, int sign) {
+    const int v = vns[begin + i], b = i / kBankBlock;
+    for (int q = 0; q < cols; ++q) {
+      const int k = colour(v, q);
+      if (k >= 0) cc.cnt[(b * cols + q) * kColours + k] += sign;
+    }
+  };
+  for (int i = 0; i < count; ++i) add(i, +1);
+  long long total = 0;
+  for (int i = 0; i < nblocks * cols; ++i) total += (i % cols == 0 ? 2 : 1) * (cc.best[i] = cc.max_of(i));
+  const long long c0 = total;
+  const std::vector<int> initial(vns.begin() + begin, vns.begin() + end);
+  Stream rng(seed);
+  const long long iters = 100ll * count;
+  std::vector<int> fresh(2 * cols);
+  for (long long it = 0; it < iters; ++it) {
+    const double T = 2.0 * (1.0 - static_cast<double>(it) / iters) + 0.02;
+    const int i1 = static_cast<int>(rng.below(count)), i2 = static_cast<int>(rng.below(count));
+    const int b1 = i1 / kBankBlock, b2 = i2 / kBankBlock;
+    if (b1 == b2) continue;
+    int old = 0;
+    for (int q = 0; q < cols; ++q) old += (q == 0 ? 2 : 1) * (cc.best[b1 * cols + q] + cc.best[b2 * cols + q]);
+    add(i1, -1);
+    add(i2, -1);
+    std::swap(vns[begin + i1], vns[begin + i2]);
+    add(i1, +1);
+    add(i2, +1);
+    int now = 0;
+    for (int q = 0; q < cols; ++q) {
+      fresh[2 * q] = cc.max_of(b1 * cols + q);
+      fresh[2 * q + 1] = cc.max_of(b2 * cols + q);
+      now += (q == 0 ? 2 : 1) * (fresh[2 * q] + fresh[2 * q + 1]);  // L load + P store
+    }
+    const int d = now - old;
+    if (d <= 0 || rng.unit() < std::exp(-d / T)) {
+      for (int q = 0; q < cols; ++q) {
+        cc.best[b1 * cols + q] = fresh[2 * q];
+        cc.best[b2 * cols + q] = fresh[2 * q + 1];
+      }
+      total += d;
+    } else {
+      add(i1, -1);
+      add(i2, -1);
+      std::swap(vns[begin + i1], vns[begin + i2]);
+      add(i1, +1);
+      add(i2, +1);
+    }
+  }
+  if (std::getenv("LDPCB_BANK_DEBUG"))
+    std::fprintf(stderr, "bank_order_vns: %d items, cost %.3f -> %.3f per block\n", count,
+                 static_cast<double>(c0) / nblocks, static_cast<double>(total) / nblocks);
+  if (total > c0) std::copy(initial.begin(), initial.end(), vns.begin() + begin);
+}
+
+}  // namespace
+
 KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, bool regular_rows) {
   if (cs < 2 + c.max_cdeg || cs % 4) throw std::invalid_argument("bad CN record stride");
   KernelTables t;
@@ -173,47 +360,68 @@ KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, boo
   if (slots >= (1ll << 30)) throw std::invalid_argument("code too large for 32-bit edge records");
   t.n_slots = static_cast<int>(slots);
   const int zero = t.n_slots - 1;
+  // groups without repeated CNs, and the VNs each group touches once
+  std::vector<std::vector<int>> group_cns(s.G);
+  std::vector<std::vector<char>> single(s.G);
+  {
+    std::vector<char> in_group(c.m, 0);
+    std::vector<int> touches(c.n, 0);
+    for (int g = 0; g < s.G; ++g) {
+      auto& cns = group_cns[g];
+      for (int i = s.grp_off[g]; i < s.grp_off[g + 1]; ++i) {
+        const int r = s.grp_cns[i];
+        if (in_group[r]) continue;
+        in_group[r] = 1;
+        cns.push_back(r);
+      }
+      for (int r : cns) {
+        in_group[r] = 0;
+        for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e) ++touches[c.cols[e]];
+      }
+      single[g].assign(c.n, 0);
+      for (int r : cns)
+        for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e) single[g][c.cols[e]] = touches[c.cols[e]] == 1;
+      for (int r : cns)
+        for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e) touches[c.cols[e]] = 0;
+    }
+  }
+  // record position of every edge (bank colouring), then its c2v slot
+  const std::vector<int> perm = bank_orders(c, group_cns, single);
+  std::vector<int> pos(c.E);
+  for (int r = 0; r < c.m; ++r)
+    for (int p = 0; p < c.row_off[r + 1] - c.row_off[r]; ++p) pos[c.row_off[r] + perm[c.row_off[r] + p]] = p;
   t.edge_slot.resize(c.E);
   for (int r = 0; r < c.m; ++r)
     for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e)
-      t.edge_slot[e] = t.slot_stride ? r * t.slot_stride + (e - c.row_off[r]) : e;
+      t.edge_slot[e] = t.slot_stride ? r * t.slot_stride + pos[e] : c.row_off[r] + pos[e];
   auto put_vn = [&](std::vector<int32_t>& out, int v) {
     out.push_back(v);
     int w = 1;
     for (int j = c.var_off[v]; j < c.var_off[v + 1]; ++j, ++w) out.push_back(t.edge_slot[c.var_edges[j]]);
     for (; w < 4 * t.vs4; ++w) out.push_back(zero);
   };
-  auto put_cn = [&](std::vector<int32_t>& out, int r, uint32_t mask) {
+  // CN record [slot of position 0, single-touch mask by position, VNs by position]
+  auto put_cn = [&](std::vector<int32_t>& out, int r, const std::vector<char>* one) {
     const int off = c.row_off[r], deg = c.row_off[r + 1] - off;
-    out.push_back(t.edge_slot[off]);
+    uint32_t mask = 0;
+    if (one)
+      for (int p = 0; p < deg; ++p)
+        if ((*one)[c.cols[off + perm[off + p]]]) mask |= 1u << p;
+    out.push_back(t.slot_stride ? r * t.slot_stride : off);
     out.push_back(static_cast<int32_t>(mask));
-    for (int k = 0; k < deg; ++k) out.push_back(c.cols[off + k]);
+    for (int p = 0; p < deg; ++p) out.push_back(c.cols[off + perm[off + p]]);
     for (int k = 2 + deg; k < t.cs; ++k) out.push_back(-1);
+    return mask;
   };
   t.cn_off.assign(1, 0);
   t.fix_off.assign(1, 0);
-  std::vector<char> in_group(c.m, 0);
   std::vector<int> touches(c.n, 0);
-  std::vector<int> cns, shared_vns;
+  std::vector<int> shared_vns;
   for (int g = 0; g < s.G; ++g) {
-    cns.clear();
-    for (int i = s.grp_off[g]; i < s.grp_off[g + 1]; ++i) {
-      const int r = s.grp_cns[i];
-      if (in_group[r]) continue;
-      in_group[r] = 1;
-      cns.push_back(r);
-    }
-    for (int r : cns) {
-      in_group[r] = 0;
+    const auto& cns = group_cns[g];
+    for (int r : cns) t.recompute |= put_cn(t.cn_rec, r, &single[g]) != 0;
+    for (int r : cns)
       for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e) ++touches[c.cols[e]];
-    }
-    for (int r : cns) {
-      uint32_t mask = 0;
-      for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e)
-        if (touches[c.cols[e]] == 1) mask |= 1u << (e - c.row_off[r]);
-      t.recompute |= mask != 0;
-      put_cn(t.cn_rec, r, mask);
-    }
     shared_vns.clear();
     for (int r : cns)
       for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e) {
@@ -226,14 +434,20 @@ KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, boo
     for (int r : cns)
       for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e) touches[c.cols[e]] = 0;
     std::sort(shared_vns.begin(), shared_vns.end());
+    if (c.max_vdeg < 16)
+      bank_order_vns(shared_vns, 0, static_cast<int>(shared_vns.size()), c, t.edge_slot, 0x66697875ull + g);
     for (int v : shared_vns) put_vn(t.fix_rec, v);
     t.cn_off.push_back(t.cn_off.back() + static_cast<int>(cns.size()));
     t.fix_off.push_back(t.fix_off.back() + static_cast<int>(shared_vns.size()));
     t.max_cn_items = std::max(t.max_cn_items, static_cast<int>(cns.size()));
     t.max_fix_items = std::max(t.max_fix_items, static_cast<int>(shared_vns.size()));
   }
-  for (int v = 0; v < c.n; ++v) put_vn(t.all_vn_rec, v);
-  for (int r = 0; r < c.m; ++r) put_cn(t.all_rec, r, 0);
+  std::vector<int> all(c.n);
+  for (int v = 0; v < c.n; ++v) all[v] = v;
+  for (int v : all) put_vn(t.all_vn_rec, v);
+  if (c.max_vdeg < 16) bank_order_vns(all, 0, c.n, c, t.edge_slot, 0x616c6cull);
+  for (int v : all) put_vn(t.tot_vn_rec, v);
+  for (int r = 0; r < c.m; ++r) put_cn(t.all_rec, r, nullptr);
   return t;
 }
 

@@ -22,7 +22,8 @@ struct DevGraph {
   const int32_t* cn_rec = nullptr;      // see host.hpp KernelTables
   const int32_t* fix_off = nullptr;     // [G+1]
   const int32_t* fix_rec = nullptr;
-  const int32_t* all_vn_rec = nullptr;  // [n] VN records
+  const int32_t* all_vn_rec = nullptr;  // [n] VN records, indexed by VN
+  const int32_t* tot_vn_rec = nullptr;  // [n] VN records in bank-coloured order
   const int32_t* all_rec = nullptr;     // [m] CN records, syndrome
   // per-frame random grouping (host.hpp ScheduleData::per_frame)
   bool per_frame = false, regroup = false, balanced = false;
