@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
   int* const s_conv = s_iters + FPC;
   int* const s_berr = s_conv + FPC;
   // staged group tables: s_go[g] = {first CN item, end, first fix-up item, end}
-  int4* const s_go = reinterpret_cast<int4*>((reinterpret_cast<uintptr_t>(s_berr + FPC) + 15) & ~uintptr_t{15});
+  int4* const s_go = reinterpret_cast<int4*>(smem + (((S + 2 * n) * FPC + 5 * FPC + 3) & ~3));
   uint16_t* const s_list = reinterpret_cast<uint16_t*>(s_go + g.G);  // RND: [FPC][slots]
   const int slots = a.list_slots;
   const int4* const all_vn = reinterpret_cast<const int4*>(g.all_vn_rec);  // indexed by VN (RND)
@@ -235,6 +235,9 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
 
   const int64_t f0 = static_cast<int64_t>(blockIdx.x) * FPC;
   const int nf = static_cast<int>(min(static_cast<int64_t>(FPC), a.frames - f0));
+#ifdef LDPCB_PHASE_TIMING
+  const long long pt_entry = clock64();
+#endif
 
   // ---- prologue: init_state (decoder.hpp:39-52) in posterior form, log2 units
   {
@@ -288,6 +291,7 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
 #ifdef LDPCB_PHASE_TIMING
   unsigned long long pt_cn = 0, pt_fix = 0, pt_end = 0, pt_groups = 0;
   const long long pt_start = clock64();
+  long long pt_loop_end = 0;
 #endif
   for (int iter = 1; iter <= a.max_iters; ++iter) {
     if constexpr (RND) {
@@ -327,19 +331,23 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
       const int4 ngo = s_go[grp + 1 < g.G ? grp + 1 : 0];  // one broadcast read, one group ahead
       int4 fix_first = make_int4(0, 0, 0, 0);
       if (j0 < xn) fix_first = __ldg(fix_vn + static_cast<size_t>(x0 + j0) * vs4);
+      // this thread's first record was loaded one group ago; the next group's
+      // is requested now, a whole CN + fix-up phase before it is needed (the
+      // records come from L2: shared memory leaves little L1)
+      const CnRecord<D, EXACT> cur = next_cn;
+      if (j0 < ngo.y - ngo.x) next_cn.load(g.cn_rec + static_cast<size_t>(ngo.x + j0) * CS);
       if (live && j0 < cn) {
         const int32_t* rec = g.cn_rec + static_cast<size_t>(c0) * CS;
         if (live == (1u << FV) - 1) {
-          cn_update<D, EXACT, FPC, FV, true>(c2v, P, next_cn, live);
+          cn_update<D, EXACT, FPC, FV, true>(c2v, P, cur, live);
           for (int j = j0 + jstep; j < cn; j += jstep)
             cn_update<D, EXACT, FPC, FV, true>(c2v, P, CnRecord<D, EXACT>(rec + j * CS), live);
         } else {
-          cn_update<D, EXACT, FPC, FV, false>(c2v, P, next_cn, live);
+          cn_update<D, EXACT, FPC, FV, false>(c2v, P, cur, live);
           for (int j = j0 + jstep; j < cn; j += jstep)
             cn_update<D, EXACT, FPC, FV, false>(c2v, P, CnRecord<D, EXACT>(rec + j * CS), live);
         }
       }
-      if (j0 < ngo.y - ngo.x) next_cn.load(g.cn_rec + static_cast<size_t>(ngo.x + j0) * CS);
       __syncthreads();
       PT_MARK(pt_b);
       pin(fix_first);
@@ -416,7 +424,9 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
     atomicAdd(&g_phase_cycles[3], static_cast<unsigned long long>(clock64() - pt_start));
     atomicAdd(&g_phase_cycles[4], pt_groups);
     atomicAdd(&g_phase_cycles[5], 1ull);
+    atomicAdd(&g_phase_cycles[6], static_cast<unsigned long long>(pt_start - pt_entry));
   }
+  pt_loop_end = clock64();
 #endif
 finish:
   __syncthreads();
@@ -485,6 +495,9 @@ finish:
     }
     for (int i = 0; i < 6; ++i) atomicAdd(a.counters + i, c[i]);
   }
+#ifdef LDPCB_PHASE_TIMING
+  if (tid == 0 && !dump) atomicAdd(&g_phase_cycles[7], static_cast<unsigned long long>(clock64() - pt_loop_end));
+#endif
 }
 
 // ---- channel: transmit_all_zero (channel.hpp:38-46), fp64 then fp32

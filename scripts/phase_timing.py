@@ -30,8 +30,8 @@ for name, s in P.configs.c1_schedules(g).items():
         e1.record()
         torch.cuda.synchronize()
         fn(buf, 1)
-        cn, fix, end, tot, groups, ctas = list(buf)[:6]
+        cn, fix, end, tot, groups, ctas, pro, epi = list(buf)[:8]
         print(f"{name} fv={fv}: {e0.elapsed_time(e1):.1f} ms plan={P.plan(g, s, F)} | per group phase: CN {cn / groups:.0f} "
               f"cyc, fix-up {fix / groups:.0f} cyc | per CTA: iteration-end {end / ctas:.0f}, total {tot / ctas:.0f} cyc, "
-              f"groups {groups / ctas:.0f}")
+              f"groups {groups / ctas:.0f}, prologue {pro / ctas:.0f}, epilogue {epi / ctas:.0f} cyc")
 P.set_tuning()
