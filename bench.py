@@ -34,7 +34,8 @@ METRIC = "decoded info bits/s at fixed iterations"
 UNIT = "info bits/s"
 MUFU_PER_EDGE = 3  # SASS-counted: 1 MUFU.EX2 + 2 MUFU.LG2 per CN-edge update (decoder.cu)
 MUFU_PER_SM_CLK = 16
-HBM_BYTES_PER_EDGE = 16  # streamed decoder: c2v read + write, posterior read + write (fp32)
+HBM_BYTES_PER_EDGE = 8  # streamed decoder: c2v read + write per CN-edge update (fp32)
+HBM_BYTES_PER_TOUCH = 8  # posterior read + write per distinct VN a group touches (fp32)
 DEFAULT_FRAMES = {"c5_n1008": 1 << 21, "c5_n64800": 8192}
 
 
@@ -277,14 +278,18 @@ def run_b200(args):
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except (OSError, ValueError):
         pass
+    # DRAM bytes of the dominant kernel: dram__bytes_read.sum + dram__bytes_write.sum per frame from the
+    # committed ncu capture of this workload (profiles/dram_bytes_per_frame.json), scaled to this launch
     traffic = None
-    tf = os.path.join(ROOT, "profiles", "dram_bytes_per_launch.json")
+    tf = os.path.join(ROOT, "profiles", "dram_bytes_per_frame.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get(args.workload)
-        except (OSError, ValueError):
+            rec = json.load(open(tf)).get(args.workload)
+            if rec:
+                traffic = rec["bytes_per_frame"] * B / 1e9
+        except (OSError, ValueError, KeyError):
             traffic = None
-    if pl["kernel"] == 1:  # shared-memory resident: SFU (MUFU) issue rate
+    if pl["kernel"] != 2:  # shared-memory resident (plan kernel 1x): SFU (MUFU) issue rate
         sm_max = float(peaks.get("sm_max_mhz", 1965.0))
         n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
         achieved = edge_updates * MUFU_PER_EDGE / (kernel_ms / 1e3)
@@ -296,15 +301,20 @@ def run_b200(args):
                             f"time {kernel_ms:.3f} ms; peak = {n_sm} SMs x {MUFU_PER_SM_CLK}/clk x {sm_max:.0f} MHz "
                             "(MEASURED_PEAKS sm_max_mhz)"}
     else:  # HBM-streamed: bytes
-        per_frame = args.iters * HBM_BYTES_PER_EDGE * s.edge_updates_per_iter + 4 * n + (n + 7) // 8
+        # SURVEY 8(d) roofline A: I x (8 E_iter + 8 T_iter) + 4n + ceil(n/8)
+        per_frame = (args.iters * (HBM_BYTES_PER_EDGE * s.edge_updates_per_iter + HBM_BYTES_PER_TOUCH * s.touched_per_iter)
+                     + 4 * n + (n + 7) // 8)
         achieved = per_frame * B / (kernel_ms / 1e3)
         peak = float(peaks.get("hbm_gbs", 6650.0)) * 1e9
         roofline = {"bound": "hbm", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": traffic,
                     "note": f"HBM-streamed decode ({pl['frames_per_cta']}-frame chunks, all its kernels): algorithmic "
-                            f"{per_frame / 1e6:.2f} MB/frame = {args.iters} iters x {HBM_BYTES_PER_EDGE} B x "
-                            f"{s.edge_updates_per_iter} CN-edge updates + LLR in + bits out, x {B} frames / "
-                            f"CUDA-event time {kernel_ms:.3f} ms; peak = MEASURED_PEAKS hbm_gbs"}
+                            f"{per_frame / 1e6:.2f} MB/frame = {args.iters} iters x ({HBM_BYTES_PER_EDGE} B x "
+                            f"{s.edge_updates_per_iter} CN-edge updates + {HBM_BYTES_PER_TOUCH} B x "
+                            f"{s.touched_per_iter} touched VNs) + LLR in + bits out, x {B} frames / CUDA-event time "
+                            f"{kernel_ms:.3f} ms; peak = MEASURED_PEAKS hbm_gbs; traffic = ncu DRAM bytes of all "
+                            "stream kernels per frame (profiles/dram_bytes_per_frame.json) x frames: below the "
+                            "algorithmic bytes because part of each group's working set is served from L2"}
 
     # ---- end to end through the host C-ABI call (pinned host buffers)
     e2e = None
