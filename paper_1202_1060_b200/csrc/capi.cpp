@@ -158,8 +158,13 @@ int make_sched(const std::shared_ptr<CodeImpl>& code, ldpcb::ScheduleData s, ldp
   impl->code = code;
   impl->host = std::move(s);
   const int bucket = ldpcb::cn_bucket(code->host.max_cdeg, code->cregular);
-  if (bucket > 0)
-    impl->tables = ldpcb::kernel_tables(code->host, impl->host, ldpcb::cn_record_stride(bucket), code->cregular);
+  if (bucket > 0) {
+    // packed 16-byte CN records (common.cuh CnRecord) where the fields fit
+    const auto& h = code->host;
+    // (the resident kernel requires them for these buckets; such codes always have n < 65536)
+    const bool packed = (bucket == 3 || bucket == 6) && h.n < 65536 && static_cast<long long>(h.m) * 7 + 1 < (1 << 24);
+    impl->tables = ldpcb::kernel_tables(h, impl->host, packed ? 4 : ldpcb::cn_record_stride(bucket), code->cregular);
+  }
   *out = new ldpcb_schedule_s{impl};
   return LDPCB_OK;
 }

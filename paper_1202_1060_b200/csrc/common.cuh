@@ -1,6 +1,7 @@
 // common.cuh -- boxplus arithmetic and table records shared by the resident
 // (shared-memory) and streamed (HBM) decoder kernels.
 #pragma once
+#include <type_traits>
 #include <cstdint>
 
 namespace ldpcb {
@@ -101,15 +102,29 @@ __device__ __forceinline__ void boxplus_row(const float (&x)[D], int deg, Store&
 }
 
 // One CN record (host.hpp KernelTables): [slot of edge 0, single-touch
-// mask, v_0 ... v_{D-1}] (v = -1 past the degree).
+// mask, v_0 ... v_{D-1}] (v = -1 past the degree), kInts ints. Regular rows
+// of degree 3 or 6 on codes with n < 65536 use the packed 16-byte form
+// (record stride cs = 4): {slot | mask << 24, v0 | v1 << 16, v2 | v3 << 16,
+// v4 | v5 << 16}, one 128-bit load instead of two.
 template <int D, bool EXACT>
 struct CnRecord {
   static constexpr int kInts = (2 + D + 3) / 4 * 4;
+  static constexpr bool kPackable = EXACT && D <= 6;
   int r[kInts];
   CnRecord() = default;
-  __device__ __forceinline__ explicit CnRecord(const int32_t* __restrict__ p) { load(p); }
-  __device__ __forceinline__ void load(const int32_t* __restrict__ p) {
+  __device__ __forceinline__ CnRecord(const int32_t* __restrict__ p, int cs) { load(p, cs); }
+  __device__ __forceinline__ void load(const int32_t* __restrict__ p, int cs) {
     const int4* q = reinterpret_cast<const int4*>(p);
+    if (kPackable && cs == 4) {
+      const int4 t = __ldg(q);
+      r[0] = t.x & 0xffffff;
+      r[1] = static_cast<int>(static_cast<unsigned>(t.x) >> 24);
+      const int w[3] = {t.y, t.z, t.w};
+#pragma unroll
+      for (int k = 0; k < D; ++k)
+        r[2 + k] = static_cast<int>((static_cast<unsigned>(w[k >> 1]) >> (16 * (k & 1))) & 0xffffu);
+      return;
+    }
 #pragma unroll
     for (int i = 0; i < kInts / 4; ++i) {
       const int4 t = __ldg(q + i);
@@ -132,6 +147,30 @@ struct CnRecord {
   }
 };
 
+
+// The packed record kept as loaded and decoded field by field at use: a
+// record prefetched a phase ahead then costs nothing until it is used.
+template <int D>
+struct CnRecordPacked {
+  static_assert(D <= 6, "packed records hold at most six 16-bit VN indices");
+  int4 w;
+  CnRecordPacked() = default;
+  __device__ __forceinline__ CnRecordPacked(const int32_t* __restrict__ p, int) { load(p, 4); }
+  __device__ __forceinline__ void load(const int32_t* __restrict__ p, int) { w = __ldg(reinterpret_cast<const int4*>(p)); }
+  __device__ __forceinline__ int slot() const { return w.x & 0xffffff; }
+  __device__ __forceinline__ unsigned mask() const { return static_cast<unsigned>(w.x) >> 24; }
+  __device__ __forceinline__ int var(int k) const {
+    const unsigned x = static_cast<unsigned>(k < 2 ? w.y : (k < 4 ? w.z : w.w));
+    return static_cast<int>((x >> (16 * (k & 1))) & 0xffffu);
+  }
+  __device__ __forceinline__ bool has(int) const { return true; }
+  __device__ __forceinline__ int deg() const { return D; }
+};
+
+// Record type of the resident kernel: packed for regular rows of degree <= 6
+// (the host packs them whenever n < 65536, always true for a resident code).
+template <int D, bool EXACT>
+using ResidentRecord = typename std::conditional<EXACT && D <= 6, CnRecordPacked<D>, CnRecord<D, EXACT>>::type;
 
 }  // namespace dev
 }  // namespace ldpcb

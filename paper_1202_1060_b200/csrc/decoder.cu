@@ -94,11 +94,15 @@ __device__ __forceinline__ void pin(int (&r)[N]) {
 #pragma unroll
   for (int i = 0; i < N; ++i) asm volatile("" : "+r"(r[i]));
 }
+template <int D, bool EXACT>
+__device__ __forceinline__ void pin_rec(CnRecord<D, EXACT>& c) { pin(c.r); }
+template <int D>
+__device__ __forceinline__ void pin_rec(CnRecordPacked<D>& c) { pin(c.w); }
 
 // live: bit i set when frame i of this thread's vector is still decoding
-template <int D, bool EXACT, int FPC, int FV, bool ALL_LIVE>
-__device__ __forceinline__ void cn_update(float* __restrict__ c2v, float* __restrict__ P,
-                                          const CnRecord<D, EXACT>& cr, unsigned live) {
+template <int D, bool EXACT, int FPC, int FV, bool ALL_LIVE, class Rec>
+__device__ __forceinline__ void cn_update(float* __restrict__ c2v, float* __restrict__ P, const Rec& cr,
+                                          unsigned live) {
   const int base = cr.slot();
   const unsigned mask = cr.mask();
   const int deg = cr.deg();
@@ -175,8 +179,8 @@ __device__ __forceinline__ void vn_sum_range(const float* __restrict__ c2v, floa
 
 // parity bit of each frame of the vector
 template <int D, bool EXACT, int FPC, int FV>
-__device__ __forceinline__ unsigned parity(const float* __restrict__ P, const int32_t* __restrict__ rec) {
-  const CnRecord<D, EXACT> cr(rec);
+__device__ __forceinline__ unsigned parity(const float* __restrict__ P, const int32_t* __restrict__ rec, int cs) {
+  const ResidentRecord<D, EXACT> cr(rec, cs);
   unsigned p = 0;
 #pragma unroll
   for (int k = 0; k < D; ++k)
@@ -208,7 +212,7 @@ template <int D, bool EXACT, int FPC, int FV, int VS, bool RND = false>
 __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode_resident(const DevGraph g,
                                                                                           const DecodeArgs a) {
   static_assert(!RND || FV == 1, "per-frame groupings need one frame per thread");
-  constexpr int CS = CnRecord<D, EXACT>::kInts;
+  const int CS = g.cs;  // CN record stride (ints): packed 4 or CnRecord::kInts
   constexpr int NG = FPC / FV;  // frame vectors per CTA
   extern __shared__ __align__(16) float smem[];
   __shared__ int s_active;
@@ -280,8 +284,9 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
   unsigned live = live_bits(fb);
   // records are prefetched one phase ahead: the first CN item of the next
   // group and the first fix-up item of the current one
-  CnRecord<D, EXACT> next_cn;
-  if (!RND && j0 < s_go[0].y - s_go[0].x) next_cn.load(g.cn_rec + static_cast<size_t>(s_go[0].x + j0) * CS);
+  using Rec = ResidentRecord<D, EXACT>;
+  Rec next_cn;
+  if (!RND && j0 < s_go[0].y - s_go[0].x) next_cn.load(g.cn_rec + static_cast<size_t>(s_go[0].x + j0) * CS, CS);
   // the current group's offsets, in registers; the next group's are read one
   // group ahead so no shared-memory read sits on the critical path
   int4 go = s_go[0];
@@ -313,13 +318,13 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
         const uint16_t* lst = s_list + fb * slots + c0;
         if (live)
           for (int j = j0; j < cn; j += jstep)
-            cn_update<D, EXACT, FPC, FV, true>(c2v, P, CnRecord<D, EXACT>(g.all_rec + lst[j] * CS), live);
+            cn_update<D, EXACT, FPC, FV, true>(c2v, P, Rec(g.all_rec + lst[j] * CS, CS), live);
         __syncthreads();
         // every VN of the group re-summed from its record (a VN shared by
         // several CNs is written several times with the same value)
         if (live)
           for (int e = j0; e < cn * D; e += jstep) {
-            const int v = __ldg(g.all_rec + lst[e / D] * CS + 2 + e % D);
+            const int v = Rec(g.all_rec + lst[e / D] * CS, CS).var(e % D);
             if (EXACT || v >= 0) vn_sum<FPC, FV, VS>(c2v, P, L, all_vn + v * vs4, vs4, __ldg(all_vn + v * vs4));
           }
         __syncthreads();
@@ -334,18 +339,18 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
       // this thread's first record was loaded one group ago; the next group's
       // is requested now, a whole CN + fix-up phase before it is needed (the
       // records come from L2: shared memory leaves little L1)
-      const CnRecord<D, EXACT> cur = next_cn;
-      if (j0 < ngo.y - ngo.x) next_cn.load(g.cn_rec + static_cast<size_t>(ngo.x + j0) * CS);
+      const Rec cur = next_cn;
+      if (j0 < ngo.y - ngo.x) next_cn.load(g.cn_rec + static_cast<size_t>(ngo.x + j0) * CS, CS);
       if (live && j0 < cn) {
         const int32_t* rec = g.cn_rec + static_cast<size_t>(c0) * CS;
         if (live == (1u << FV) - 1) {
           cn_update<D, EXACT, FPC, FV, true>(c2v, P, cur, live);
           for (int j = j0 + jstep; j < cn; j += jstep)
-            cn_update<D, EXACT, FPC, FV, true>(c2v, P, CnRecord<D, EXACT>(rec + j * CS), live);
+            cn_update<D, EXACT, FPC, FV, true>(c2v, P, Rec(rec + j * CS, CS), live);
         } else {
           cn_update<D, EXACT, FPC, FV, false>(c2v, P, cur, live);
           for (int j = j0 + jstep; j < cn; j += jstep)
-            cn_update<D, EXACT, FPC, FV, false>(c2v, P, CnRecord<D, EXACT>(rec + j * CS), live);
+            cn_update<D, EXACT, FPC, FV, false>(c2v, P, Rec(rec + j * CS, CS), live);
         }
       }
       __syncthreads();
@@ -361,7 +366,7 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
         }
         __syncthreads();
       }
-      pin(next_cn.r);
+      pin_rec(next_cn);
       go = ngo;
 #ifdef LDPCB_PHASE_TIMING
       const long long pt_c = clock64();
@@ -384,7 +389,7 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
     if (live) {
       int w[FV] = {};
       for (int j = j0; j < m; j += jstep) {
-        const unsigned p = parity<D, EXACT, FPC, FV>(P, g.all_rec + j * CS);
+        const unsigned p = parity<D, EXACT, FPC, FV>(P, g.all_rec + j * CS, CS);
 #pragma unroll
         for (int i = 0; i < FV; ++i) w[i] += (p >> i) & 1u;
       }

@@ -351,7 +351,8 @@ void bank_order_vns(std::vector<int>& vns, int begin, int end, const CodeData& c
 }  // namespace
 
 KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, bool regular_rows) {
-  if (cs < 2 + c.max_cdeg || cs % 4) throw std::invalid_argument("bad CN record stride");
+  const bool packed = cs == 4 && regular_rows && c.max_cdeg <= 6 && c.n < 65536;  // common.cuh CnRecord
+  if ((!packed && cs < 2 + c.max_cdeg) || cs % 4) throw std::invalid_argument("bad CN record stride");
   KernelTables t;
   t.cs = cs;
   t.vs4 = (1 + c.max_vdeg + 3) / 4;
@@ -407,7 +408,15 @@ KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, boo
     if (one)
       for (int p = 0; p < deg; ++p)
         if ((*one)[c.cols[off + perm[off + p]]]) mask |= 1u << p;
-    out.push_back(t.slot_stride ? r * t.slot_stride : off);
+    const int slot = t.slot_stride ? r * t.slot_stride : off;
+    if (packed) {  // {slot | mask << 24, v0 | v1 << 16, v2 | v3 << 16, v4 | v5 << 16}
+      uint32_t w[4] = {static_cast<uint32_t>(slot) | (mask << 24), 0, 0, 0};
+      for (int p = 0; p < deg; ++p)
+        w[1 + p / 2] |= static_cast<uint32_t>(c.cols[off + perm[off + p]]) << (16 * (p & 1));
+      for (uint32_t x : w) out.push_back(static_cast<int32_t>(x));
+      return mask;
+    }
+    out.push_back(slot);
     out.push_back(static_cast<int32_t>(mask));
     for (int p = 0; p < deg; ++p) out.push_back(c.cols[off + perm[off + p]]);
     for (int k = 2 + deg; k < t.cs; ++k) out.push_back(-1);

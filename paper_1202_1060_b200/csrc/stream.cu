@@ -80,8 +80,7 @@ __global__ void stream_init(int n, const float* __restrict__ llr, ChunkState s) 
 
 // CN phase of one group over (record, quad) items.
 template <int D, bool EXACT>
-__global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ recs, int count, ChunkState s) {
-  constexpr int CS = CnRecord<D, EXACT>::kInts;
+__global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ recs, int CS, int count, ChunkState s) {
   const int64_t QB = s.B / 4;
   const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (item >= count * QB) return;
@@ -89,7 +88,7 @@ __global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ rec
   const int64_t q = item - j * QB;
   const int4 dn = *reinterpret_cast<const int4*>(s.done + 4 * q);
   if (dn.x & dn.y & dn.z & dn.w) return;
-  const CnRecord<D, EXACT> cr(recs + static_cast<int64_t>(j) * CS);
+  const CnRecord<D, EXACT> cr(recs + static_cast<int64_t>(j) * CS, CS);
   const int base = cr.slot();
   const unsigned mask = cr.mask();
   const int deg = cr.deg();
@@ -167,15 +166,14 @@ __global__ void __launch_bounds__(256) stream_vnsum(const int4* __restrict__ rec
 
 // Syndrome weight per frame (decoder.hpp:129-137) over (CN, quad) items.
 template <int D, bool EXACT>
-__global__ void __launch_bounds__(256) stream_syndrome(const int32_t* __restrict__ recs, int m, ChunkState s) {
-  constexpr int CS = CnRecord<D, EXACT>::kInts;
+__global__ void __launch_bounds__(256) stream_syndrome(const int32_t* __restrict__ recs, int CS, int m, ChunkState s) {
   const int64_t QB = s.B / 4;
   const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (item >= m * QB) return;
   const int r = static_cast<int>(item / QB);
   const int64_t q = item - r * QB;
   if (quad_done(s, q)) return;
-  const CnRecord<D, EXACT> cr(recs + static_cast<int64_t>(r) * CS);
+  const CnRecord<D, EXACT> cr(recs + static_cast<int64_t>(r) * CS, CS);
   unsigned p = 0;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
@@ -293,8 +291,8 @@ __global__ void stream_dump(const DevGraph g, ChunkState s, float* c2v_out, floa
 }
 
 struct StreamKernels {
-  void (*cn)(const int32_t*, int, ChunkState);
-  void (*syn)(const int32_t*, int, ChunkState);
+  void (*cn)(const int32_t*, int, int, ChunkState);
+  void (*syn)(const int32_t*, int, int, ChunkState);
 };
 
 StreamKernels pick(const DevGraph& g) {
@@ -383,7 +381,7 @@ int launch_stream(const DevGraph& g, const DecodeArgs& a, void* stream_v, Plan* 
         ++sub;
         const int c0 = g.h_cn_off[grp], cn = g.h_cn_off[grp + 1] - c0;
         if (cn > 0) {
-          K.cn<<<blocks_for(cn * QB, tpb), tpb, 0, st>>>(g.cn_rec + static_cast<size_t>(c0) * g.cs, cn, s);
+          K.cn<<<blocks_for(cn * QB, tpb), tpb, 0, st>>>(g.cn_rec + static_cast<size_t>(c0) * g.cs, g.cs, cn, s);
           ++launches;
         }
         const int x0 = g.h_fix_off[grp], xn = g.h_fix_off[grp + 1] - x0;
@@ -401,7 +399,7 @@ int launch_stream(const DevGraph& g, const DecodeArgs& a, void* stream_v, Plan* 
         ++launches;
       }
       if (!check) continue;
-      K.syn<<<blocks_for(g.m * QB, tpb), tpb, 0, st>>>(g.all_rec, g.m, s);
+      K.syn<<<blocks_for(g.m * QB, tpb), tpb, 0, st>>>(g.all_rec, g.cs, g.m, s);
       stream_iter_end<<<blocks_for(s.nb, tpb), tpb, 0, st>>>(s, iter, a.early_stop, a.trace, a.max_iters, f0);
       launches += 2;
     }
