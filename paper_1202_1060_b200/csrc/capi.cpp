@@ -103,7 +103,7 @@ struct SchedImpl {
   ldpcb::KernelTables tables;
   std::mutex mu;
   struct Dev {
-    int32_t *cn_off, *cn_rec, *fix_off, *fix_rec, *all_vn_rec, *tot_vn_rec, *all_rec, *edge_slot;
+    int32_t *cn_off, *cn_rec, *fix_off, *fix_rec, *all_vn_rec, *tot_vn_rec, *all_rec, *edge_slot, *vn_pos;
     std::vector<void*> ptrs;
   };
   std::map<int, Dev> dev;
@@ -126,7 +126,8 @@ struct SchedImpl {
     x.tot_vn_rec = upload(tables.tot_vn_rec);
     x.all_rec = upload(tables.all_rec);
     x.edge_slot = upload(tables.edge_slot);
-    x.ptrs = {x.cn_off, x.cn_rec, x.fix_off, x.fix_rec, x.all_vn_rec, x.tot_vn_rec, x.all_rec, x.edge_slot};
+    x.vn_pos = upload(tables.vn_pos);
+    x.ptrs = {x.cn_off, x.cn_rec, x.fix_off, x.fix_rec, x.all_vn_rec, x.tot_vn_rec, x.all_rec, x.edge_slot, x.vn_pos};
     return dev.emplace(d, std::move(x)).first->second;
   }
 };
@@ -217,6 +218,7 @@ ldpcb::DevGraph dev_graph(ldpcb_code code, ldpcb_schedule s) {
   g.max_fix_items = t.max_fix_items;
   g.cols = c.cols;
   g.edge_slot = d.edge_slot;
+  g.vn_pos = d.vn_pos;
   g.cn_off = d.cn_off;
   g.cn_rec = d.cn_rec;
   g.fix_off = d.fix_off;

@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
   {
     const float* llr = a.llr + f0 * n;
     for (int i = tid; i < nf * n; i += nt) {
-      const int ff = i / n, v = i - ff * n;
+      const int ff = i / n, v = __ldg(g.vn_pos + (i - ff * n));
       const float x = clamp_llr(__ldg(llr + i)) * kLog2e;
       smem[(S + v) * FPC + ff] = x;
       smem[(S + n + v) * FPC + ff] = x;
@@ -445,7 +445,8 @@ finish:
       for (int e = j0; e < E; e += jstep) {
         const float c = c2v[__ldg(g.edge_slot + e) * FPC + i];
         if (a.c2v_out) a.c2v_out[(f0 + fb + i) * E + e] = c * kLn2;
-        if (a.v2c_out) a.v2c_out[(f0 + fb + i) * E + e] = clamp_bits(P[__ldg(g.cols + e) * FPC + i] - c) * kLn2;
+        if (a.v2c_out)
+          a.v2c_out[(f0 + fb + i) * E + e] = clamp_bits(P[__ldg(g.vn_pos + __ldg(g.cols + e)) * FPC + i] - c) * kLn2;
       }
     }
     return;
@@ -464,21 +465,21 @@ finish:
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int v = b * 8 + j;
-          if (v < n && P[v * FPC + i] < 0.f) byte |= 1u << j;
+          if (v < n && P[__ldg(g.vn_pos + v) * FPC + i] < 0.f) byte |= 1u << j;
         }
         out[b] = static_cast<uint8_t>(byte);
         errs += __popc(byte);
       }
     } else if (a.bits || a.counters || a.bit_errors) {
       for (int v = j0; v < n; v += jstep) {
-        const int bit = P[v * FPC + i] < 0.f;
+        const int bit = P[__ldg(g.vn_pos + v) * FPC + i] < 0.f;
         if (a.bits) a.bits[(f0 + f) * n + v] = static_cast<uint8_t>(bit);
         errs += bit;
       }
     }
     if (errs) atomicAdd(&s_berr[f], errs);
     if (a.posterior)
-      for (int v = j0; v < n; v += jstep) a.posterior[(f0 + f) * n + v] = P[v * FPC + i] * kLn2;
+      for (int v = j0; v < n; v += jstep) a.posterior[(f0 + f) * n + v] = P[__ldg(g.vn_pos + v) * FPC + i] * kLn2;
   }
   if (tid < nf) {
     const int it = a.early_stop ? s_iters[tid] : a.max_iters;

@@ -97,8 +97,8 @@ struct ScheduleData {
 // check-regular codes slot(m, k) = m * slot_stride + k with an ODD stride, so
 // the consecutive CNs of a window hit distinct shared-memory banks; otherwise
 // slot = CN-major edge id. The last slot is always zero (pads VN records).
-//   CN record  [slot of edge 0, single-touch mask, v_0 .. v_{d-1}, -1 ...]  cs ints
-//   VN record  [v, slot_0 .. slot_{d-1} (ascending CN), zero slot ...]    4*vs4 ints
+//   CN record  [slot of edge 0, single-touch mask, pos(v_0) .. pos(v_{d-1}), -1 ...]  cs ints
+//   VN record  [pos(v), slot_0 .. slot_{d-1} (ascending CN), zero slot ...] 4*vs4 ints
 // Bit k of the mask is set when v_k has no other CN in the group: the CN
 // thread then updates that VN's posterior in place; VNs shared by two or more
 // CNs of the group ("fix" records) are re-summed after the CN phase.
@@ -111,10 +111,13 @@ struct KernelTables {
   bool recompute = false;  // some CN updates a posterior in place
   std::vector<int32_t> cn_off, cn_rec;    // per group
   std::vector<int32_t> fix_off, fix_rec;  // per group: VNs shared by >= 2 CNs
-  std::vector<int32_t> all_vn_rec;        // every VN, record v = VN v (decoder.hpp:162-165)
+  std::vector<int32_t> all_vn_rec;        // every VN, record p = the VN at position p (decoder.hpp:162-165)
   std::vector<int32_t> tot_vn_rec;        // the same records in bank-coloured order (exact totals)
   std::vector<int32_t> all_rec;           // every CN in index order (syndrome)
   std::vector<int32_t> edge_slot;         // CN-major edge id -> slot
+  // VN v lives at position vn_pos[v] of the kernels' per-VN arrays (P, L):
+  // every record holds positions, not VN ids (bank colouring relabels VNs)
+  std::vector<int32_t> vn_pos;
   int max_cn_items = 0, max_fix_items = 0;
 };
 

@@ -194,13 +194,29 @@ struct ColourCells {
   }
 };
 
-// perm[off + p] = original edge index (relative to the row) at record position p
-std::vector<int> bank_orders(const CodeData& c, const std::vector<std::vector<int>>& group_cns,
-                             const std::vector<std::vector<char>>& single) {
-  std::vector<int> perm(c.E);
+// Layout chosen by the annealer below: the record order of every CN's edges
+// and the shared-memory colour of every VN.
+struct BankLayout {
+  std::vector<int> perm;    // perm[off + p] = original edge index (relative to the row) at record position p
+  std::vector<int> colour;  // colour[v] = shared-memory position of VN v mod 16
+};
+
+// Joint annealing of (1) the edge order inside each CN (boxplus is
+// symmetric) and (2) the colour of each VN: its position in the P / L arrays
+// is colour + 16 * rank, so colour classes keep the sizes of v mod 16 and
+// the positions stay a permutation of [0, n). Moves swap two edges of a CN
+// or the colours of two VNs.
+BankLayout bank_layout(const CodeData& c, const std::vector<std::vector<int>>& group_cns,
+                       const std::vector<std::vector<char>>& single) {
+  BankLayout L;
+  L.perm.resize(c.E);
+  L.colour.resize(c.n);
   for (int r = 0; r < c.m; ++r)
-    for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e) perm[e] = e - c.row_off[r];
-  if (c.n > 32768 || c.m < 2) return perm;
+    for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e) L.perm[e] = e - c.row_off[r];
+  for (int v = 0; v < c.n; ++v) L.colour[v] = v % kColours;
+  if (c.n > 32768 || c.m < 2) return L;
+  std::vector<int>& perm = L.perm;
+  std::vector<int>& col = L.colour;
   const int D = c.max_cdeg;
   // (group, block) of every CN occurrence
   struct Occ {
@@ -214,81 +230,121 @@ std::vector<int> bank_orders(const CodeData& c, const std::vector<std::vector<in
       if (j % kBankBlock == 0) ++nblocks;
       occ[group_cns[g][j]].push_back({(nblocks - 1) * 2 * D, g});
     }
-  ColourCells cc(nblocks * 2 * D, 2 * D);
+  const int ncells = nblocks * 2 * D;
+  // per cell: colour counts, a histogram of those counts and their maximum,
+  // so every increment / decrement updates the total cost in O(1)
+  constexpr int H = kBankBlock * 4 + 1;
+  std::vector<uint8_t> cnt(static_cast<size_t>(ncells) * kColours, 0);
+  std::vector<uint16_t> hist(static_cast<size_t>(ncells) * H, 0);
+  std::vector<uint8_t> mx(ncells, 0);
+  for (int i = 0; i < ncells; ++i) hist[static_cast<size_t>(i) * H] = kColours;
+  long long total = 0;
+  auto bump = [&](int cell, int k, int sign) {
+    uint8_t& x = cnt[static_cast<size_t>(cell) * kColours + k];
+    uint16_t* h = &hist[static_cast<size_t>(cell) * H];
+    --h[x];
+    x = static_cast<uint8_t>(x + sign);
+    ++h[x];
+    if (sign > 0 && x > mx[cell]) {
+      mx[cell] = x;
+      ++total;
+    } else if (sign < 0 && h[mx[cell]] == 0) {
+      --mx[cell];
+      --total;
+    }
+  };
+  // position of edge e inside its row's record (inverse of perm)
+  std::vector<int> rpos(c.E), row_of(c.E);
+  for (int r = 0; r < c.m; ++r)
+    for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e) {
+      rpos[c.row_off[r] + perm[e]] = e - c.row_off[r];
+      row_of[e] = r;
+    }
   auto vn_at = [&](int r, int p) { return c.cols[c.row_off[r] + perm[c.row_off[r] + p]]; };
-  auto add = [&](int r, int p, int sign) {
-    const int v = vn_at(r, p), col = v % kColours;
+  auto add = [&](int r, int p, int v, int sign) {
+    const int k = col[v];
     for (const Occ& o : occ[r]) {
-      cc.cnt[(o.cell0 + p) * kColours + col] += sign;
-      if (single[o.group][v]) cc.cnt[(o.cell0 + D + p) * kColours + col] += sign;
+      bump(o.cell0 + p, k, sign);
+      if (single[o.group][v]) bump(o.cell0 + D + p, k, sign);
     }
   };
   for (int r = 0; r < c.m; ++r)
-    for (int p = 0; p < c.row_off[r + 1] - c.row_off[r]; ++p) add(r, p, +1);
-  long long total = 0;
-  for (int i = 0; i < nblocks * 2 * D; ++i) total += cc.best[i] = cc.max_of(i);
+    for (int p = 0; p < c.row_off[r + 1] - c.row_off[r]; ++p) add(r, p, vn_at(r, p), +1);
   const long long c0 = total;
-  const std::vector<int> initial = perm;  // structured codes (QC) may start out conflict-free
+  const BankLayout initial = L;  // structured codes (QC) may start out conflict-free
   Stream rng(0x6c64706362616e6bull);
   static const long long scale = [] {
     const char* e = std::getenv("LDPCB_BANK_ITERS");  // moves per CN; tuning / A-B only
-    return e ? std::atoll(e) : 1000ll;
+    return e ? std::atoll(e) : 4000ll;
   }();
-  const long long iters = std::min<long long>(8000000, scale * c.m);
-  auto cells_of = [&](int r, int p1, int p2, int* out) {
-    int k = 0;
-    for (const Occ& o : occ[r]) {
-      out[k++] = o.cell0 + p1;
-      out[k++] = o.cell0 + p2;
-      out[k++] = o.cell0 + D + p1;
-      out[k++] = o.cell0 + D + p2;
-    }
-    return k;
-  };
-  int cl[64];
-  for (long long it = 0; it < iters; ++it) {
-    const double T = 2.0 * (1.0 - static_cast<double>(it) / iters) + 0.02;
-    const int r = static_cast<int>(rng.below(c.m));
-    const int deg = c.row_off[r + 1] - c.row_off[r];
-    if (deg < 2 || occ[r].empty() || occ[r].size() > 16) continue;
-    const int p1 = static_cast<int>(rng.below(deg));
-    int p2 = static_cast<int>(rng.below(deg - 1));
-    if (p2 >= p1) ++p2;
-    const int nc = cells_of(r, p1, p2, cl);
-    int old = 0;
-    for (int i = 0; i < nc; ++i) old += cc.best[cl[i]];
-    add(r, p1, -1);
-    add(r, p2, -1);
+  const long long iters = std::min<long long>(20000000, scale * c.m);
+  auto swap_edges = [&](int r, int p1, int p2) {
+    const int v1 = vn_at(r, p1), v2 = vn_at(r, p2);
+    add(r, p1, v1, -1);
+    add(r, p2, v2, -1);
     std::swap(perm[c.row_off[r] + p1], perm[c.row_off[r] + p2]);
-    add(r, p1, +1);
-    add(r, p2, +1);
-    int now = 0, fresh[64];
-    for (int i = 0; i < nc; ++i) now += fresh[i] = cc.max_of(cl[i]);
-    const int d = now - old;
-    if (d <= 0 || rng.unit() < std::exp(-d / T)) {
-      for (int i = 0; i < nc; ++i) cc.best[cl[i]] = fresh[i];
-      total += d;
-    } else {
-      add(r, p1, -1);
-      add(r, p2, -1);
-      std::swap(perm[c.row_off[r] + p1], perm[c.row_off[r] + p2]);
-      add(r, p1, +1);
-      add(r, p2, +1);
+    rpos[c.row_off[r] + perm[c.row_off[r] + p1]] = p1;
+    rpos[c.row_off[r] + perm[c.row_off[r] + p2]] = p2;
+    add(r, p1, v2, +1);
+    add(r, p2, v1, +1);
+  };
+  auto vn_add = [&](int v, int sign) {
+    for (int j = c.var_off[v]; j < c.var_off[v + 1]; ++j) {
+      const int e = c.var_edges[j];
+      add(row_of[e], rpos[e], v, sign);
+    }
+  };
+  auto swap_colours = [&](int v1, int v2) {
+    vn_add(v1, -1);
+    vn_add(v2, -1);
+    std::swap(col[v1], col[v2]);
+    vn_add(v1, +1);
+    vn_add(v2, +1);
+  };
+  long long best_total = total;
+  BankLayout best = L;
+  for (long long it = 0; it < iters; ++it) {
+    const double T = 1.0 * (1.0 - static_cast<double>(it) / iters) + 0.02;
+    const long long before = total;
+    if (rng.below(2) == 0) {  // swap two edges of a CN
+      const int r = static_cast<int>(rng.below(c.m));
+      const int deg = c.row_off[r + 1] - c.row_off[r];
+      if (deg < 2 || occ[r].empty() || occ[r].size() > 16) continue;
+      const int p1 = static_cast<int>(rng.below(deg));
+      int p2 = static_cast<int>(rng.below(deg - 1));
+      if (p2 >= p1) ++p2;
+      swap_edges(r, p1, p2);
+      const long long d = total - before;
+      if (d > 0 && rng.unit() >= std::exp(-d / T)) swap_edges(r, p1, p2);
+    } else {  // swap the colours of two VNs
+      const int v1 = static_cast<int>(rng.below(c.n)), v2 = static_cast<int>(rng.below(c.n));
+      if (col[v1] == col[v2]) continue;
+      swap_colours(v1, v2);
+      const long long d = total - before;
+      if (d > 0 && rng.unit() >= std::exp(-d / T)) swap_colours(v1, v2);
+    }
+    if (total < best_total && it > iters / 2) {
+      best_total = total;
+      best = L;
     }
   }
+  if (total > best_total) {
+    L = best;
+    total = best_total;
+  }
   if (std::getenv("LDPCB_BANK_DEBUG"))
-    std::fprintf(stderr, "bank_orders: %d cells, cost %.3f -> %.3f per cell (%lld moves)\n", nblocks * 2 * D,
-                 static_cast<double>(c0) / (nblocks * 2 * D), static_cast<double>(total) / (nblocks * 2 * D), iters);
-  return total <= c0 ? perm : initial;
+    std::fprintf(stderr, "bank_layout: %d cells, cost %.3f -> %.3f per cell (%lld moves)\n", ncells,
+                 static_cast<double>(c0) / ncells, static_cast<double>(total) / ncells, iters);
+  return total <= c0 ? L : initial;
 }
 
 void bank_order_vns(std::vector<int>& vns, int begin, int end, const CodeData& c, const std::vector<int>& edge_slot,
-                    uint64_t seed) {
+                    const std::vector<int>& vcol, uint64_t seed) {
   const int count = end - begin;
   if (count <= kBankBlock || c.n > 32768) return;
   const int cols = 1 + c.max_vdeg;
   auto colour = [&](int v, int q) {  // q = 0: L/P of v, else the (q-1)-th c2v slot (-1: none)
-    if (q == 0) return v % kColours;
+    if (q == 0) return vcol[v];
     const int j = c.var_off[v] + q - 1;
     return j < c.var_off[v + 1] ? edge_slot[c.var_edges[j]] % kColours : -1;
   };
@@ -387,7 +443,15 @@ KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, boo
     }
   }
   // record position of every edge (bank colouring), then its c2v slot
-  const std::vector<int> perm = bank_orders(c, group_cns, single);
+  const BankLayout lay = bank_layout(c, group_cns, single);
+  const std::vector<int>& perm = lay.perm;
+  // shared-memory position of every VN: colour + 16 * rank inside its colour
+  t.vn_pos.resize(c.n);
+  {
+    std::vector<int> rank(kColours, 0);
+    for (int v = 0; v < c.n; ++v) t.vn_pos[v] = lay.colour[v] + kColours * rank[lay.colour[v]]++;
+  }
+  const std::vector<int32_t>& vp = t.vn_pos;
   std::vector<int> pos(c.E);
   for (int r = 0; r < c.m; ++r)
     for (int p = 0; p < c.row_off[r + 1] - c.row_off[r]; ++p) pos[c.row_off[r] + perm[c.row_off[r] + p]] = p;
@@ -396,7 +460,7 @@ KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, boo
     for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e)
       t.edge_slot[e] = t.slot_stride ? r * t.slot_stride + pos[e] : c.row_off[r] + pos[e];
   auto put_vn = [&](std::vector<int32_t>& out, int v) {
-    out.push_back(v);
+    out.push_back(vp[v]);
     int w = 1;
     for (int j = c.var_off[v]; j < c.var_off[v + 1]; ++j, ++w) out.push_back(t.edge_slot[c.var_edges[j]]);
     for (; w < 4 * t.vs4; ++w) out.push_back(zero);
@@ -412,13 +476,13 @@ KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, boo
     if (packed) {  // {slot | mask << 24, v0 | v1 << 16, v2 | v3 << 16, v4 | v5 << 16}
       uint32_t w[4] = {static_cast<uint32_t>(slot) | (mask << 24), 0, 0, 0};
       for (int p = 0; p < deg; ++p)
-        w[1 + p / 2] |= static_cast<uint32_t>(c.cols[off + perm[off + p]]) << (16 * (p & 1));
+        w[1 + p / 2] |= static_cast<uint32_t>(vp[c.cols[off + perm[off + p]]]) << (16 * (p & 1));
       for (uint32_t x : w) out.push_back(static_cast<int32_t>(x));
       return mask;
     }
     out.push_back(slot);
     out.push_back(static_cast<int32_t>(mask));
-    for (int p = 0; p < deg; ++p) out.push_back(c.cols[off + perm[off + p]]);
+    for (int p = 0; p < deg; ++p) out.push_back(vp[c.cols[off + perm[off + p]]]);
     for (int k = 2 + deg; k < t.cs; ++k) out.push_back(-1);
     return mask;
   };
@@ -444,17 +508,20 @@ KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, boo
       for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e) touches[c.cols[e]] = 0;
     std::sort(shared_vns.begin(), shared_vns.end());
     if (c.max_vdeg < 16)
-      bank_order_vns(shared_vns, 0, static_cast<int>(shared_vns.size()), c, t.edge_slot, 0x66697875ull + g);
+      bank_order_vns(shared_vns, 0, static_cast<int>(shared_vns.size()), c, t.edge_slot, lay.colour,
+                     0x66697875ull + g);
     for (int v : shared_vns) put_vn(t.fix_rec, v);
     t.cn_off.push_back(t.cn_off.back() + static_cast<int>(cns.size()));
     t.fix_off.push_back(t.fix_off.back() + static_cast<int>(shared_vns.size()));
     t.max_cn_items = std::max(t.max_cn_items, static_cast<int>(cns.size()));
     t.max_fix_items = std::max(t.max_fix_items, static_cast<int>(shared_vns.size()));
   }
+  // all_vn_rec is indexed by shared-memory position (the per-frame kernel
+  // looks records up by the positions in its CN records)
   std::vector<int> all(c.n);
-  for (int v = 0; v < c.n; ++v) all[v] = v;
+  for (int v = 0; v < c.n; ++v) all[vp[v]] = v;
   for (int v : all) put_vn(t.all_vn_rec, v);
-  if (c.max_vdeg < 16) bank_order_vns(all, 0, c.n, c, t.edge_slot, 0x616c6cull);
+  if (c.max_vdeg < 16) bank_order_vns(all, 0, c.n, c, t.edge_slot, lay.colour, 0x616c6cull);
   for (int v : all) put_vn(t.tot_vn_rec, v);
   for (int r = 0; r < c.m; ++r) put_cn(t.all_rec, r, nullptr);
   return t;

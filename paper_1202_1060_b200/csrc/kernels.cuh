@@ -18,6 +18,7 @@ struct DevGraph {
   int max_cn_items = 0, max_fix_items = 0;
   const int32_t* cols = nullptr;        // CSR columns (state dumps)
   const int32_t* edge_slot = nullptr;   // edge id -> c2v slot (state dumps)
+  const int32_t* vn_pos = nullptr;      // [n] VN id -> position in the per-VN state arrays
   const int32_t* cn_off = nullptr;      // [G+1] CN record offsets per group
   const int32_t* cn_rec = nullptr;      // see host.hpp KernelTables
   const int32_t* fix_off = nullptr;     // [G+1]

@@ -50,7 +50,7 @@ __device__ __forceinline__ bool quad_done(const ChunkState& s, int64_t q) {
 
 // L = P = clamp(llr) in log2 units, transposed [nb][n] -> [n][B] through a
 // 32 x 32 shared-memory tile; padding frames (>= nb) are marked done.
-__global__ void stream_init(int n, const float* __restrict__ llr, ChunkState s) {
+__global__ void stream_init(int n, const int32_t* __restrict__ pos, const float* __restrict__ llr, ChunkState s) {
   __shared__ float tile[32][33];
   const int v0 = blockIdx.x * 32, f0 = blockIdx.y * 32;
   for (int r = threadIdx.y; r < 32; r += blockDim.y) {
@@ -62,8 +62,9 @@ __global__ void stream_init(int n, const float* __restrict__ llr, ChunkState s) 
     const int v = v0 + r, f = f0 + threadIdx.x;
     if (v < n && f < s.B) {
       const float x = tile[threadIdx.x][r];
-      s.L[static_cast<int64_t>(v) * s.B + f] = x;
-      s.P[static_cast<int64_t>(v) * s.B + f] = x;
+      const int64_t row = __ldg(pos + v);
+      s.L[row * s.B + f] = x;
+      s.P[row * s.B + f] = x;
     }
   }
   if (blockIdx.x == 0 && threadIdx.y == 0) {
@@ -203,7 +204,8 @@ __global__ void stream_iter_end(ChunkState s, int iter, int early_stop, int32_t*
 // Hard decisions (tie -> 0): packed or byte bits, per-frame error counts and
 // optional posteriors, transposed [n][B] -> [frames][...] through shared
 // memory. Block (32, 8): tile of 32 frames x 256 VNs.
-__global__ void stream_bits(int n, ChunkState s, uint8_t* bits, int packed, float* posterior, int64_t frame0) {
+__global__ void stream_bits(int n, const int32_t* __restrict__ pos, ChunkState s, uint8_t* bits, int packed, float* posterior,
+                            int64_t frame0) {
   __shared__ unsigned char tile[32][33];
   __shared__ float ptile[32][33];
   const int f0 = blockIdx.y * 32, b0 = blockIdx.x * 32;  // 32 bytes = 256 VNs
@@ -215,7 +217,7 @@ __global__ void stream_bits(int n, ChunkState s, uint8_t* bits, int packed, floa
     if (f < s.nb && b < nbytes)
       for (int j = 0; j < 8; ++j) {
         const int v = 8 * b + j;
-        if (v < n && s.P[static_cast<int64_t>(v) * s.B + f] < 0.f) byte |= 1u << j;
+        if (v < n && s.P[static_cast<int64_t>(__ldg(pos + v)) * s.B + f] < 0.f) byte |= 1u << j;
       }
     tile[threadIdx.x][r] = static_cast<unsigned char>(byte);
     errs += __popc(byte);
@@ -243,7 +245,7 @@ __global__ void stream_bits(int n, ChunkState s, uint8_t* bits, int packed, floa
       __syncthreads();
       for (int r = threadIdx.y; r < 32; r += blockDim.y) {
         const int v = vb + r, f = f0 + threadIdx.x;
-        ptile[r][threadIdx.x] = (v < n && f < s.B) ? s.P[static_cast<int64_t>(v) * s.B + f] * kLn2 : 0.f;
+        ptile[r][threadIdx.x] = (v < n && f < s.B) ? s.P[static_cast<int64_t>(__ldg(pos + v)) * s.B + f] * kLn2 : 0.f;
       }
       __syncthreads();
       for (int r = threadIdx.y; r < 32; r += blockDim.y) {
@@ -287,7 +289,7 @@ __global__ void stream_dump(const DevGraph g, ChunkState s, float* c2v_out, floa
   const float c = s.c2v[static_cast<int64_t>(__ldg(g.edge_slot + e)) * s.B + f];
   if (c2v_out) c2v_out[(frame0 + f) * g.E + e] = c * kLn2;
   if (v2c_out)
-    v2c_out[(frame0 + f) * g.E + e] = clamp_bits(s.P[static_cast<int64_t>(__ldg(g.cols + e)) * s.B + f] - c) * kLn2;
+    v2c_out[(frame0 + f) * g.E + e] = clamp_bits(s.P[static_cast<int64_t>(__ldg(g.vn_pos + __ldg(g.cols + e))) * s.B + f] - c) * kLn2;
 }
 
 struct StreamKernels {
@@ -364,7 +366,7 @@ int launch_stream(const DevGraph& g, const DecodeArgs& a, void* stream_v, Plan* 
     err = cudaMemsetAsync(s.c2v, 0, 4ull * g.n_slots * B, st);
     if (err != cudaSuccess) break;
     stream_init<<<dim3((g.n + 31) / 32, static_cast<unsigned>((B + 31) / 32)), dim3(32, 8), 0, st>>>(
-        g.n, a.llr + f0 * g.n, s);
+        g.n, g.vn_pos, a.llr + f0 * g.n, s);
     ++launches;
     if (a.trace) {
       err = cudaMemsetAsync(a.trace + f0 * a.max_iters, 0xff, 4ull * s.nb * a.max_iters, st);
@@ -413,7 +415,7 @@ int launch_stream(const DevGraph& g, const DecodeArgs& a, void* stream_v, Plan* 
     } else {
       const int nbytes = (g.n + 7) / 8;
       stream_bits<<<dim3((nbytes + 31) / 32, static_cast<unsigned>((B + 31) / 32)), dim3(32, 8), 0, st>>>(
-          g.n, s, a.bits, a.bits_packed, a.posterior, f0);
+          g.n, g.vn_pos, s, a.bits, a.bits_packed, a.posterior, f0);
       stream_final<<<blocks_for(s.nb, tpb), tpb, 0, st>>>(s, a, f0);
       launches += 2;
     }
