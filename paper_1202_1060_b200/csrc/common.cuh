@@ -101,6 +101,116 @@ __device__ __forceinline__ void boxplus_row(const float (&x)[D], int deg, Store&
   emit(0, sn, sd);
 }
 
+// ---- two frames per instruction: sm_100 packed fp32 (FADD2 / FMUL2 / FFMA2)
+// The same arithmetic as boxplus_row on a pair of frames held as one 64-bit
+// register pair, so every add / mul / fma issues once for both frames (each
+// lane rounds exactly like the scalar instruction: results are bit-identical).
+using f32x2 = unsigned long long;
+__device__ __forceinline__ f32x2 pack2(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float lo2(f32x2 t) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(t));
+  return a;
+}
+__device__ __forceinline__ float hi2(f32x2 t) {
+  float a, b;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(t));
+  return b;
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f32x2 sub2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// a * b rounded once, as fma(a, b, -0) with the -0 pair read from constant
+// memory: ptxas contracts mul.rn.f32x2 (and an fma with a literal -0 addend)
+// into a following add.rn.f32x2, unlike the scalar .rn forms, which would
+// break the symmetric rounding boxplus relies on; an fma whose addend it
+// cannot see is never fused.
+static __constant__ unsigned long long c_negzero2 = 0x8000000080000000ull;
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+  f32x2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c_negzero2));
+  return r;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+// boxplus_row for two frames at once: x[k] packs frame 0 (low) and frame 1
+// (high); store(k, c2v_k) receives packed outputs. Same operation order and
+// rounding as boxplus_row, lane by lane.
+template <int D, bool EXACT, class Store>
+__device__ __forceinline__ void boxplus_row_x2(const f32x2 (&x)[D], int deg, Store&& store) {
+  f32x2 z[D];
+  unsigned sa = 0, sb = 0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    if (EXACT || k < deg) {
+      const float a = lo2(x[k]), b = hi2(x[k]);
+      sa ^= __float_as_uint(a);
+      sb ^= __float_as_uint(b);
+      z[k] = pack2(mufu_ex2(-fminf(fabsf(a), kClampB)), mufu_ex2(-fminf(fabsf(b), kClampB)));
+    } else {
+      z[k] = 0ull;  // (0.f, 0.f): boxplus identity (N, D) = (0, 1)
+    }
+  }
+  const f32x2 one = pack2(1.f, 1.f);
+  auto emit = [&](int k, f32x2 num, f32x2 den) {
+    if (EXACT || k < deg) {
+      const f32x2 dd = sub2(pack2(mufu_lg2(lo2(den)), mufu_lg2(hi2(den))), pack2(mufu_lg2(lo2(num)), mufu_lg2(hi2(num))));
+      const unsigned ta = sa ^ __float_as_uint(lo2(x[k])), tb = sb ^ __float_as_uint(hi2(x[k]));
+      store(k, pack2(__uint_as_float((__float_as_uint(lo2(dd)) & 0x7fffffffu) | (ta & 0x80000000u)),
+                     __uint_as_float((__float_as_uint(hi2(dd)) & 0x7fffffffu) | (tb & 0x80000000u))));
+    }
+  };
+  f32x2 pn[D > 1 ? D - 1 : 1], pd[D > 1 ? D - 1 : 1];
+  pn[0] = z[0];
+  pd[0] = one;
+#pragma unroll
+  for (int k = 1; k < D - 1; ++k) {
+    pn[k] = fma2(z[k], pd[k - 1], pn[k - 1]);
+    pd[k] = fma2(z[k], pn[k - 1], pd[k - 1]);
+  }
+  emit(D - 1, pn[D - 2], pd[D - 2]);
+  f32x2 sn = z[D - 1], sd = one;
+  if (D >= 3) {
+    constexpr int k = D >= 3 ? D - 2 : 1;
+    emit(k, add2(pn[k - 1], mul2(sn, pd[k - 1])), add2(pd[k - 1], mul2(pn[k - 1], sn)));
+    const f32x2 tn = add2(z[k], sn);
+    const f32x2 td = fma2(z[k], sn, one);
+    sn = tn;
+    sd = td;
+  }
+#pragma unroll
+  for (int k = D - 3; k >= 2; --k) {
+    emit(k, add2(mul2(pn[k - 1], sd), mul2(sn, pd[k - 1])), add2(mul2(pd[k - 1], sd), mul2(pn[k - 1], sn)));
+    const f32x2 tn = fma2(z[k], sd, sn);
+    const f32x2 td = fma2(z[k], sn, sd);
+    sn = tn;
+    sd = td;
+  }
+  if (D >= 4) {
+    emit(1, add2(mul2(pn[0], sd), sn), add2(sd, mul2(pn[0], sn)));
+    const f32x2 tn = fma2(z[1], sd, sn);
+    const f32x2 td = fma2(z[1], sn, sd);
+    sn = tn;
+    sd = td;
+  }
+  emit(0, sn, sd);
+}
+
 // One CN record (host.hpp KernelTables): [slot of edge 0, single-touch
 // mask, v_0 ... v_{D-1}] (v = -1 past the degree), kInts ints. Regular rows
 // of degree 3 or 6 on codes with n < 65536 use the packed 16-byte form

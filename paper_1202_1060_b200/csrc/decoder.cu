@@ -117,16 +117,37 @@ __device__ __forceinline__ void cn_update(float* __restrict__ c2v, float* __rest
       for (int i = 0; i < FV; ++i) pv[k].v[i] = old[k].v[i] = 0.f;
     }
   }
+  if constexpr (FV == 2) {  // both frames per packed fp32 instruction
+    f32x2 x[D];
 #pragma unroll
-  for (int i = 0; i < FV; ++i) {
-    float x[D];
-#pragma unroll
-    for (int k = 0; k < D; ++k) x[k] = pv[k].v[i] - old[k].v[i];
-    boxplus_row<D, EXACT>(x, deg, [&](int k, float c) {
-      out[k].v[i] = (ALL_LIVE || (live & (1u << i))) ? c : old[k].v[i];
-      // in-place posterior: P + (c - old) = v2c + c (v2c = P - old, unclamped)
-      pv[k].v[i] = (ALL_LIVE || (live & (1u << i))) ? x[k] + c : pv[k].v[i];
+    for (int k = 0; k < D; ++k) x[k] = sub2(pack2(pv[k].v[0], pv[k].v[1]), pack2(old[k].v[0], old[k].v[1]));
+    boxplus_row_x2<D, EXACT>(x, deg, [&](int k, f32x2 c) {
+      const f32x2 p = add2(x[k], c);  // in-place posterior: v2c + c
+      if (ALL_LIVE || (live & 1u)) {
+        out[k].v[0] = lo2(c);
+        pv[k].v[0] = lo2(p);
+      } else {
+        out[k].v[0] = old[k].v[0];
+      }
+      if (ALL_LIVE || (live & 2u)) {
+        out[k].v[1] = hi2(c);
+        pv[k].v[1] = hi2(p);
+      } else {
+        out[k].v[1] = old[k].v[1];
+      }
     });
+  } else {
+#pragma unroll
+    for (int i = 0; i < FV; ++i) {
+      float x[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) x[k] = pv[k].v[i] - old[k].v[i];
+      boxplus_row<D, EXACT>(x, deg, [&](int k, float c) {
+        out[k].v[i] = (ALL_LIVE || (live & (1u << i))) ? c : old[k].v[i];
+        // in-place posterior: P + (c - old) = v2c + c (v2c = P - old, unclamped)
+        pv[k].v[i] = (ALL_LIVE || (live & (1u << i))) ? x[k] + c : pv[k].v[i];
+      });
+    }
   }
 #pragma unroll
   for (int k = 0; k < D; ++k) {
@@ -145,8 +166,14 @@ __device__ __forceinline__ void vn_sum(const float* __restrict__ c2v, float* __r
   FVec<FV> acc = lds<FV>(L + v * FPC);
   auto add = [&](int slot) {
     const FVec<FV> c = lds<FV>(c2v + slot * FPC);
+    if constexpr (FV == 2) {
+      const f32x2 t = add2(pack2(acc.v[0], acc.v[1]), pack2(c.v[0], c.v[1]));
+      acc.v[0] = lo2(t);
+      acc.v[1] = hi2(t);
+    } else {
 #pragma unroll
-    for (int i = 0; i < FV; ++i) acc.v[i] += c.v[i];
+      for (int i = 0; i < FV; ++i) acc.v[i] += c.v[i];
+    }
   };
   add(t.y);
   add(t.z);
