@@ -631,8 +631,8 @@ using KernelFn = void (*)(const DevGraph, const DecodeArgs);
 
 template <int D, bool EXACT, int VS>
 KernelFn pick_fpc(int fpc, int fv) {
-  if (fv == 2 && D <= 8) {
-    switch (fpc) {
+  if constexpr (D <= 8) {
+    if (fv == 2) switch (fpc) {
       case 2: return decode_resident<D, EXACT, 2, 2, VS>;
       case 4: return decode_resident<D, EXACT, 4, 2, VS>;
       case 8: return decode_resident<D, EXACT, 8, 2, VS>;
