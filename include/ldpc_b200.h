@@ -120,6 +120,11 @@ int ldpcb_sigma2_from_ebn0(double ebn0_db, double rate, double *sigma2);
  * device with the reference's stream (rng.hpp) in fp64, stored as fp32 */
 int ldpcb_channel_llr_device(int n, double sigma2, uint64_t seed, int64_t frame0, int64_t frames, float *d_llr,
                              void *stream);
+/* xoshiro256 state of frame `frame`'s noise stream, Rng(mix_seed(seed, frame))
+ * (rng.hpp:19-46, channel.hpp:40), after `draws` 64-bit draws, by jump-ahead
+ * (x^draws mod the generator's characteristic polynomial). The device
+ * channel starts segments of long frames this way; exposed for tests. */
+int ldpcb_channel_stream_state(uint64_t seed, uint64_t frame, uint64_t draws, uint64_t state[4]);
 
 /* ---- decoding (decode, decoder.hpp:143-181) ------------------------------ */
 

@@ -488,6 +488,19 @@ int ldpcb_channel_llr_device(int n, double sigma2, uint64_t seed, int64_t frame0
   });
 }
 
+int ldpcb_channel_stream_state(uint64_t seed, uint64_t frame, uint64_t draws, uint64_t* state) {
+  return guard([&] {
+    need(state != nullptr, "null state buffer");
+    ldpcb::Stream st(ldpcb::stream_seed(seed, frame));
+    ldpcb::stream_jump(st, ldpcb::stream_jump_poly(draws));
+    state[0] = st.w0;
+    state[1] = st.w1;
+    state[2] = st.w2;
+    state[3] = st.w3;
+    return LDPCB_OK;
+  });
+}
+
 int ldpcb_decode_device(ldpcb_code code, ldpcb_schedule s, int64_t frames, const float* d_llr, int max_iters,
                         int early_stop, uint8_t* d_bits, int bits_packed, int32_t* d_iterations, uint8_t* d_converged,
                         float* d_posterior, int32_t* d_trace, int64_t* d_counters, void* stream) {

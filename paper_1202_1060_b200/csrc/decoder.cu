@@ -31,8 +31,11 @@
 #include <atomic>
 #include <map>
 #include <mutex>
+#include <tuple>
+#include <vector>
 
 #include "common.cuh"
+#include "host.hpp"
 #include "kernels.cuh"
 #include "rng.cuh"
 
@@ -543,6 +546,50 @@ __global__ void channel_kernel(int n, double sigma, double scale, uint64_t seed,
   for (int i = 0; i < n; ++i) out[i] = static_cast<float>(scale * (1.0 + sigma * rng.normal()));
 }
 
+// Segment-parallel channel for long frames: thread (frame, segment s)
+// starts its frame's stream advanced by s * L draws (polys[s - 1] = x^(s L)
+// mod p, host_rng.cpp) and produces normals [s L, s L + L). L is even, so a
+// segment starts on a Box-Muller pair and each normal pairs the same two
+// draws as the sequential stream (cos first, sin cached): identical LLRs.
+__global__ void channel_seg_kernel(int n, int L, int S, double sigma, double scale, uint64_t seed, int64_t frame0,
+                                   int64_t frames, const uint64_t* __restrict__ polys, float* __restrict__ llr) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= frames * S) return;
+  const int64_t f = t / S;
+  const int s = static_cast<int>(t - f * S);
+  Stream rng(stream_seed(seed, static_cast<uint64_t>(frame0 + f)));
+  if (s > 0) {  // jump(): xor of the states at the set coefficients
+    const uint64_t* poly = polys + 4 * (s - 1);
+    uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    for (int w = 0; w < 4; ++w) {
+      const uint64_t word = __ldg(poly + w);
+      for (int b = 0; b < 64; ++b) {
+        if ((word >> b) & 1u) {
+          a0 ^= rng.w0;
+          a1 ^= rng.w1;
+          a2 ^= rng.w2;
+          a3 ^= rng.w3;
+        }
+        rng.u64();
+      }
+    }
+    rng.w0 = a0;
+    rng.w1 = a1;
+    rng.w2 = a2;
+    rng.w3 = a3;
+  }
+  const int i0 = s * L, i1 = min(n, i0 + L);
+  float* out = llr + f * n;
+  for (int i = i0; i < i1; i += 2) {  // Stream::normal(), both halves of a pair
+    const double a = rng.unit();
+    const double b = rng.unit();
+    const double r = sqrt(-2.0 * log(a));
+    const double th = 6.283185307179586476925286766559 * b;
+    out[i] = static_cast<float>(scale * (1.0 + sigma * (r * cos(th))));
+    if (i + 1 < i1) out[i + 1] = static_cast<float>(scale * (1.0 + sigma * (r * sin(th))));
+  }
+}
+
 // ---- one CN per thread on explicit inputs (check_update KATs)
 template <int D, bool EXACT>
 __global__ void check_update_kernel(int deg, int64_t rows, const float* __restrict__ v2c, float* __restrict__ c2v) {
@@ -864,10 +911,58 @@ extern "C" int ldpcb_debug_phase_cycles(unsigned long long* out, int reset) {
 }
 #endif
 
+// Jump polynomials x^(s L) mod p for s = 1 .. S-1, uploaded once per
+// (device, L, S) and kept for the process lifetime (a few KB each).
+const uint64_t* channel_polys(int L, int S) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int>, uint64_t*> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(dev, L, S);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  std::vector<uint64_t> h(4ull * (S - 1));
+  for (int s = 1; s < S; ++s) {
+    const auto p = stream_jump_poly(static_cast<uint64_t>(s) * L);
+    std::copy(p.begin(), p.end(), h.begin() + 4 * (s - 1));
+  }
+  uint64_t* d = nullptr;
+  if (cudaMalloc(&d, h.size() * 8) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(d, h.data(), h.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(d);
+    return nullptr;
+  }
+  cache[key] = d;
+  return d;
+}
+
 int launch_channel(int n, double sigma2, uint64_t seed, int64_t frame0, int64_t frames, float* llr, void* stream) {
   if (frames <= 0) return 0;
   const double sigma = std::sqrt(sigma2);  // channel.hpp:41-42
   const double scale = 2.0 / sigma2;
+  // Long frames in small batches: split each frame's stream into S segments
+  // (jump-ahead) so that about 1024 threads per SM generate noise.
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t want = static_cast<int64_t>(sms) * 1024;
+  int S = static_cast<int>(std::min<int64_t>((want + frames - 1) / frames, n / 256));
+  if (S >= 2) {
+    const int L = ((n + S - 1) / S + 1) & ~1;  // even segment length
+    S = (n + L - 1) / L;
+    const uint64_t* polys = channel_polys(L, S);
+    if (!polys) return static_cast<int>(cudaErrorMemoryAllocation);
+    const int tpb = 128;
+    const int64_t blocks = (frames * S + tpb - 1) / tpb;
+    channel_seg_kernel<<<static_cast<unsigned>(blocks), tpb, 0, static_cast<cudaStream_t>(stream)>>>(
+        n, L, S, sigma, scale, seed, frame0, frames, polys, llr);
+    ++g_launches;
+    return static_cast<int>(cudaGetLastError());
+  }
   const int tpb = 128;
   const int64_t blocks = (frames + tpb - 1) / tpb;
   channel_kernel<<<static_cast<unsigned>(blocks), tpb, 0, static_cast<cudaStream_t>(stream)>>>(

@@ -13,6 +13,7 @@
 //   random_groups <- detail::generate_groups      schedule.hpp:54-115
 //   iteration_budget / measure_cocsg              schedule.hpp:175-210
 #pragma once
+#include <array>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -133,5 +134,12 @@ ScheduleData per_frame_schedule(const CodeData& c, Kind kind, int G, double over
 Rows random_groups(int M, int G, double overlap, uint64_t stream_seed_value);
 int iteration_budget(const ScheduleData& s, int n_checks, int i_max);
 std::vector<int> measure_cocsg(const CodeData& c, const ScheduleData& s);
+
+// Jump-ahead of the channel stream (host_rng.cpp): coefficients of
+// x^draws mod p(x), p the characteristic polynomial of xoshiro256, and their
+// application to a stream state (the published jump() loop).
+struct Stream;
+std::array<uint64_t, 4> stream_jump_poly(uint64_t draws);
+void stream_jump(Stream& st, const std::array<uint64_t, 4>& poly);
 
 }  // namespace ldpcb

@@ -1,4 +1,5 @@
-"""Device channel (transmit_all_zero) cost next to the decode it feeds."""
+"""Device channel throughput (normals/s) for the BASELINE frame lengths at the
+batch sizes the Monte-Carlo harness uses."""
 import sys
 
 import torch
@@ -6,25 +7,15 @@ import torch
 sys.path.insert(0, ".")
 import paper_1202_1060_b200 as P  # noqa: E402
 
-
-def timeit(fn, reps=3):
-    fn()
+for n, frames in ((1008, 1 << 20), (1944, 1 << 19), (64800, 1024), (64800, 8192)):
+    x = torch.empty((frames, n), dtype=torch.float32, device="cuda")
+    P.transmit_all_zero(n, 0.63, 1, 0, frames, out=x)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(reps):
-        fn()
+    for _ in range(3):
+        P.transmit_all_zero(n, 0.63, 1, 0, frames, out=x)
     e1.record()
     torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / reps
-
-
-for name, g, s, F, it in (("C1", P.configs.c1_code(), None, 1 << 20, 10),
-                          ("C4", P.configs.c4_code(), None, 8192, 10)):
-    s = (P.configs.c1_schedules(g) if name == "C1" else P.configs.c4_schedules(g))["ndgsbp"]
-    s2 = P.sigma2_from_ebn0(2.0, g.rate)
-    x = torch.empty((F, g.n_vars), dtype=torch.float32, device="cuda")
-    ch = timeit(lambda: P.transmit_all_zero(g.n_vars, s2, 1, 0, F, out=x))
-    dec = timeit(lambda: P.decode_batch(g, s, x, it, early_stop=False, packed=True))
-    sim = timeit(lambda: P.simulate(g, s, s2, 1, 0, F, it, early_stop=False))
-    print(f"{name}: channel {ch:.2f} ms, decode {dec:.2f} ms, simulate {sim:.2f} ms for {F} frames")
+    ms = e0.elapsed_time(e1) / 3
+    print(f"n={n} frames={frames}: {ms:.2f} ms, {frames * n / ms / 1e6:.3f} G normals/s, {frames / ms * 1e3:.3e} frames/s")

@@ -215,10 +215,13 @@ def test_syndrome_is_exact_on_output_bits(P, torch, orc):
 
 
 def test_device_channel_bit_exact(P, torch, orc):
-    for n, ebn0, seed, f0 in ((1008, 2.0, 1, 0), (1001, 0.5, 7, 12345), (64, 4.0, 99, 2**33)):
+    # the last cases are long frames in small batches: each frame's stream is
+    # split into segments started by jump-ahead (decoder.cu channel_seg_kernel)
+    for n, ebn0, seed, f0, frames in ((1008, 2.0, 1, 0, 300), (1001, 0.5, 7, 12345, 300), (64, 4.0, 99, 2**33, 300),
+                                      (64800, 1.1, 3, 5, 40), (20001, 0.9, 11, 2**40, 7), (1944, 1.5, 2, 0, 3)):
         s2 = P.sigma2_from_ebn0(ebn0, 0.5)
-        d = P.transmit_all_zero(n, s2, seed, f0, 300).cpu().numpy()
-        h = orc.transmit_batch_f32(s2, seed, n, f0, 300, THREADS)
+        d = P.transmit_all_zero(n, s2, seed, f0, frames).cpu().numpy()
+        h = orc.transmit_batch_f32(s2, seed, n, f0, frames, THREADS)
         assert np.array_equal(d, h), (n, np.abs(d - h).max())
 
 

@@ -179,3 +179,59 @@ def test_decode_argument_errors_without_gpu(P):
         _lib.check(_lib.lib.ldpcb_decode_host(g.handle, so.handle, 1, None, 5, 1, None, 0, None, None, None, None, None))
     with pytest.raises(ValueError):
         P.set_tuning(3, 0)
+
+
+def _py_stream(seed, frame):
+    """Pure-Python restatement of Rng(mix_seed(seed, frame)) (rng.hpp:10-46)."""
+    M = (1 << 64) - 1
+
+    def splitmix(st):
+        st = (st + 0x9E3779B97F4A7C15) & M
+        z = st
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+        return st, z ^ (z >> 31)
+
+    st, a = splitmix(seed)
+    st ^= (0xD1342543DE82EF95 * (frame + 1)) & M
+    _, b = splitmix(st)
+    st = a ^ b
+    w = []
+    for _ in range(4):
+        st, z = splitmix(st)
+        w.append(z)
+    return w
+
+
+def _py_step(w):
+    M = (1 << 64) - 1
+    w0, w1, w2, w3 = w
+    t = (w1 << 17) & M
+    w2 ^= w0
+    w3 ^= w1
+    w1 ^= w2
+    w0 ^= w3
+    w2 ^= t
+    w3 = ((w3 << 45) | (w3 >> 19)) & M
+    return [w0, w1, w2, w3]
+
+
+def test_channel_stream_jump_ahead_matches_stepping(P):
+    """The jump-ahead the device channel uses to start frame segments
+    (host_rng.cpp) lands on the same xoshiro256 state as stepping draw by
+    draw, at every distance (segment starts are multiples of an even L)."""
+    import ctypes as C
+
+    lib = P.api.lib
+    lib.ldpcb_channel_stream_state.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64)]
+    for seed, frame in ((1, 0), (7, 12345), (2**63 + 5, 2**33)):
+        w = _py_stream(seed, frame)
+        targets = sorted({0, 1, 2, 255, 256, 257, 1000, 4097, 30000})
+        done = 0
+        for d in targets:
+            while done < d:
+                w = _py_step(w)
+                done += 1
+            out = (C.c_uint64 * 4)()
+            assert lib.ldpcb_channel_stream_state(seed, frame, d, out) == 0
+            assert list(out) == w, (seed, frame, d)
