@@ -276,11 +276,34 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode
   // ---- prologue: init_state (decoder.hpp:39-52) in posterior form, log2 units
   {
     const float* llr = a.llr + f0 * n;
-    for (int i = tid; i < nf * n; i += nt) {
+    auto put = [&](int i, float raw) {  // element i of the CTA's frames -> P and L
       const int ff = i / n, v = __ldg(g.vn_pos + (i - ff * n));
-      const float x = clamp_llr(__ldg(llr + i)) * kLog2e;
+      const float x = clamp_llr(raw) * kLog2e;
       smem[(S + v) * FPC + ff] = x;
       smem[(S + n + v) * FPC + ff] = x;
+    };
+    if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(a.llr) & 15) == 0) {
+      // 16-byte loads, four per thread in flight before any is used
+      constexpr int U = 4;
+      const float4* l4 = reinterpret_cast<const float4*>(llr);
+      const int nv = nf * n / 4;
+      for (int b0 = tid; b0 < nv; b0 += U * nt) {
+        float4 x[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (b0 + u * nt < nv) x[u] = __ldg(l4 + b0 + u * nt);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (b0 + u * nt < nv) {
+            const int i = 4 * (b0 + u * nt);
+            put(i, x[u].x);
+            put(i + 1, x[u].y);
+            put(i + 2, x[u].z);
+            put(i + 3, x[u].w);
+          }
+      }
+    } else {
+      for (int i = tid; i < nf * n; i += nt) put(i, __ldg(llr + i));
     }
     for (int i = nf * n + tid; i < FPC * n; i += nt) {  // padding frames: saturated zero codeword
       const int ff = i / n, v = i - ff * n;
