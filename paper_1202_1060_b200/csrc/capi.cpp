@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <chrono>
 #include <cstring>
@@ -186,6 +187,34 @@ void retain_pool_memory() {
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
   }
   done[dev] = true;
+}
+
+// Host-buffer entry points work on two non-blocking streams per (host
+// thread, device) that live as long as the thread: stream-ordered pool
+// allocations freed on them are reused by the next call without fresh
+// physical mappings (a new stream per call made every multi-GB chunk
+// allocation map new memory and serialised the copy/decode pipeline).
+struct HostStreams {
+  std::map<int, std::array<cudaStream_t, 2>> by_dev;
+  ~HostStreams() {
+    for (auto& kv : by_dev)
+      for (cudaStream_t st : kv.second) cudaStreamDestroy(st);  // errors ignored at teardown
+  }
+  cudaStream_t get(int k) {
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    auto it = by_dev.find(dev);
+    if (it == by_dev.end()) {
+      std::array<cudaStream_t, 2> st{};
+      for (auto& x : st) cuda_check(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking), "cudaStreamCreate");
+      it = by_dev.emplace(dev, st).first;
+    }
+    return it->second[k];
+  }
+};
+cudaStream_t host_stream(int k) {
+  thread_local HostStreams streams;
+  return streams.get(k);
 }
 
 void check_pair(ldpcb_code code, ldpcb_schedule s) {
@@ -549,7 +578,7 @@ int ldpcb_decode_host(ldpcb_code code, ldpcb_schedule s, int64_t frames, const f
     int64_t chunk = p0.kernel == 2 ? std::max<int64_t>(4, (p0.fpc / 2 + 3) / 4 * 4)
                                    : std::max<int64_t>(p0.fpc, (int64_t{32} << 20) / (4 * n));
     chunk = std::min<int64_t>(chunk, frames);
-    chunk = (chunk + p0.fpc - 1) / p0.fpc * p0.fpc;
+    if (p0.kernel != 2) chunk = (chunk + p0.fpc - 1) / p0.fpc * p0.fpc;  // whole CTAs (streamed: fpc = chunk)
     const int kSlots = 2;
     cudaStream_t st[kSlots];
     struct Buf {
@@ -562,7 +591,7 @@ int ldpcb_decode_host(ldpcb_code code, ldpcb_schedule s, int64_t frames, const f
       int64_t* cnt = nullptr;
     } buf[kSlots];
     for (int k = 0; k < kSlots; ++k) {
-      cuda_check(cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking), "cudaStreamCreate");
+      st[k] = host_stream(k);
       cuda_check(cudaMallocAsync(&buf[k].llr, chunk * n * sizeof(float), st[k]), "cudaMallocAsync");
       if (bits) cuda_check(cudaMallocAsync(&buf[k].bits, chunk * nb, st[k]), "cudaMallocAsync");
       if (iterations) cuda_check(cudaMallocAsync(&buf[k].it, chunk * sizeof(int32_t), st[k]), "cudaMallocAsync");
@@ -625,7 +654,6 @@ int ldpcb_decode_host(ldpcb_code code, ldpcb_schedule s, int64_t frames, const f
       if (buf[k].trace) cudaFreeAsync(buf[k].trace, st[k]);
       if (buf[k].cnt) cudaFreeAsync(buf[k].cnt, st[k]);
       cuda_check(cudaStreamSynchronize(st[k]), "sync");
-      cudaStreamDestroy(st[k]);
     }
     if (counters)
       for (int i = 0; i < 6; ++i) counters[i] += total[i];
@@ -711,8 +739,7 @@ int ldpcb_run_sweep_host(ldpcb_code code, ldpcb_schedule s, const double* ebn0_d
     const double rate = static_cast<double>(h.n - h.m) / h.n;
     int64_t cap = wave_frames > 0 ? wave_frames : (int64_t{1} << 20);
     cap = std::min(cap, max_frames);
-    cudaStream_t st;
-    cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+    cudaStream_t st = host_stream(0);
     int32_t *d_be = nullptr, *d_it = nullptr;
     uint8_t* d_cv = nullptr;
     std::vector<int32_t> be(cap), it(cap);
@@ -722,7 +749,6 @@ int ldpcb_run_sweep_host(ldpcb_code code, ldpcb_schedule s, const double* ebn0_d
       if (d_it) cudaFreeAsync(d_it, st);
       if (d_cv) cudaFreeAsync(d_cv, st);
       cudaStreamSynchronize(st);
-      cudaStreamDestroy(st);
     };
     try {
       cuda_check(cudaMallocAsync(&d_be, cap * 4, st), "cudaMallocAsync");
@@ -785,8 +811,7 @@ int ldpcb_simulate_host(ldpcb_code code, ldpcb_schedule s, double sigma2, uint64
   return guard([&] {
     check_pair(code, s);
     need(counters != nullptr, "null counters");
-    cudaStream_t st;
-    cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+    cudaStream_t st = host_stream(0);
     int64_t* d = nullptr;
     int rc = LDPCB_OK;
     try {
@@ -802,13 +827,11 @@ int ldpcb_simulate_host(ldpcb_code code, ldpcb_schedule s, double sigma2, uint64
     } catch (...) {
       if (d) cudaFreeAsync(d, st);
       cudaStreamSynchronize(st);
-      cudaStreamDestroy(st);
       throw;
     }
     const std::string err = g_last_error;  // keep the inner message
     cudaFreeAsync(d, st);
     cudaStreamSynchronize(st);
-    cudaStreamDestroy(st);
     g_last_error = err;
     return rc;
   });
