@@ -1,13 +1,16 @@
 #!/bin/bash
 # Full GPU evidence run: tests, both bench workloads, launch lists, ncu captures.
+# Launch lists are taken at the bench's own batch sizes per decode (C1: 65536-frame
+# decodes; C4: one 8192-frame chunk) so DRAM bytes per frame match the bench line.
 set -x
 mkdir -p gpurun_out
 python -m pytest tests -m gpu -q 2>&1 | tail -5
 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_c5_n1008.json 2> gpurun_out/bench_c5_n1008.err; cat gpurun_out/bench_c5_n1008.json
 python bench.py --workload c5_n64800 --steps 5 --warmup 2 > gpurun_out/bench_c5_n64800.json 2> gpurun_out/bench_c5_n64800.err; cat gpurun_out/bench_c5_n64800.json
 python bench.py --impl reference --steps 2 --warmup 0 > gpurun_out/ref_c5_n1008.json 2>&1; cat gpurun_out/ref_c5_n1008.json
+python bench.py --impl reference --workload c5_n64800 --steps 2 --warmup 0 > gpurun_out/ref_c5_n64800.json 2>&1; cat gpurun_out/ref_c5_n64800.json
 S1="python bench.py --frames 65536 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
-S2="python bench.py --workload c5_n64800 --frames 1024 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
+S2="python bench.py --workload c5_n64800 --frames 8192 --steps 1 --warmup 0 --no-cpu-baseline --no-e2e"
 $S1 > gpurun_out/s1.log 2>&1 && ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_c5_n1008.csv $S1 > /dev/null 2>&1
 $S2 > gpurun_out/s2.log 2>&1 && ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_c5_n64800.csv $S2 > /dev/null 2>&1
 $S1 > gpurun_out/s3.log 2>&1 && ncu --set full --clock-control none --import-source on -k regex:decode_resident -s 1 -c 1 -f -o gpurun_out/prof_resident $S1 > gpurun_out/ncu1.log 2>&1
