@@ -571,7 +571,7 @@ int ldpcb_decode_host(ldpcb_code code, ldpcb_schedule s, int64_t frames, const f
     const auto g = dev_graph(code, s);
     const int n = g.n;
     const int64_t nb = bits_packed ? (n + 7) / 8 : n;
-    const ldpcb::Plan p0 = ldpcb::plan_decode(g, frames);
+    const ldpcb::Plan p0 = ldpcb::plan_decode(g, frames, early_stop != 0);
     if (p0.kernel == 0) throw std::runtime_error("no decoder plan for this code (check degree or memory)");
     // chunks of ~32 MB of LLRs, a multiple of the frames per CTA; for the
     // streamed kernel two half-size decode chunks so copies overlap decoding
@@ -673,7 +673,7 @@ void simulate_frames(ldpcb_code code, ldpcb_schedule s, double sigma2, uint64_t 
   need(sigma2 > 0.0, "sigma2 must be positive");
   if (frames == 0) return;
   const auto g = dev_graph(code, s);
-  const ldpcb::Plan p0 = ldpcb::plan_decode(g, frames);
+  const ldpcb::Plan p0 = ldpcb::plan_decode(g, frames, early_stop != 0);
   if (p0.kernel == 0) throw std::runtime_error("no decoder plan for this code (check degree or memory)");
   auto st = static_cast<cudaStream_t>(stream);
   int64_t chunk = std::max<int64_t>(p0.fpc, (int64_t{256} << 20) / (4 * g.n));

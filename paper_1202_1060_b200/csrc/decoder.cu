@@ -109,6 +109,20 @@ __device__ __forceinline__ void cn_update(float* __restrict__ c2v, float* __rest
   const int base = cr.slot();
   const unsigned mask = cr.mask();
   const int deg = cr.deg();
+  if constexpr (FV == 1) {
+    // one frame: v2c in registers only; every output is stored as the
+    // boxplus emits it (keeps wide rows, D = 16 / 32, within the register file)
+    if (!ALL_LIVE && !(live & 1u)) return;
+    float x[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) x[k] = cr.has(k) ? P[cr.var(k) * FPC] - c2v[(base + k) * FPC] : 0.f;
+    boxplus_row<D, EXACT>(x, deg, [&](int k, float c) {
+      c2v[(base + k) * FPC] = c;
+      // in-place posterior: P + (c - old) = v2c + c (v2c = P - old, unclamped)
+      if (mask & (1u << k)) P[cr.var(k) * FPC] = x[k] + c;
+    });
+    return;
+  }
   FVec<FV> pv[D], old[D], out[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) {
@@ -239,7 +253,7 @@ __device__ unsigned long long g_phase_cycles[8];
 // the CN records are the per-CN ones (no in-place posterior updates) and
 // after every CN phase each edge of the group re-sums its VN exactly.
 template <int D, bool EXACT, int FPC, int FV, int VS, bool RND = false>
-__global__ void __launch_bounds__(max_threads_for(D, FV), D <= 8 ? 2 : 1) decode_resident(const DevGraph g,
+__global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decode_resident(const DevGraph g,
                                                                                           const DecodeArgs a) {
   static_assert(!RND || FV == 1, "per-frame groupings need one frame per thread");
   const int CS = g.cs;  // CN record stride (ints): packed 4 or CnRecord::kInts
@@ -790,7 +804,7 @@ void set_force_kernel(int kernel) { g_force_kernel = kernel; }
 void set_lazy_totals(int on) { g_lazy_totals = on; }
 int lazy_totals() { return g_lazy_totals.load(); }
 
-Plan plan_resident(const DevGraph& g, int64_t frames);
+Plan plan_resident(const DevGraph& g, int64_t frames, bool early_stop);
 
 int launch_gen_groups(const DevGraph& g, int64_t frame0, int64_t frames, int list0, int n_lists, uint16_t* out,
                       void* stream) {
@@ -815,48 +829,90 @@ int launch_gen_groups(const DevGraph& g, int64_t frame0, int64_t frames, int lis
   return static_cast<int>(cudaGetLastError());
 }
 
-Plan plan_decode(const DevGraph& g, int64_t frames) {
-  if (g.per_frame) return plan_resident(g, frames);  // per-frame groups: resident kernel only
+Plan plan_decode(const DevGraph& g, int64_t frames, bool early_stop) {
+  if (g.per_frame) return plan_resident(g, frames, early_stop);  // per-frame groups: resident kernel only
   if (g_force_kernel.load() == 2) return plan_stream(g, frames);
-  Plan p = plan_resident(g, frames);
+  Plan p = plan_resident(g, frames, early_stop);
   if (p.kernel == 0 && g_force_kernel.load() != 1) p = plan_stream(g, frames);
   return p;
 }
 
-Plan plan_resident(const DevGraph& g, int64_t frames) {
+// Registers per thread of a kernel instantiation (cached per function).
+int kernel_regs(KernelFn fn) {
+  static std::mutex mu;
+  static std::map<const void*, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(reinterpret_cast<const void*>(fn));
+  if (it != cache.end()) return it->second;
+  cudaFuncAttributes at{};
+  const int r = cudaFuncGetAttributes(&at, reinterpret_cast<const void*>(fn)) == cudaSuccess ? at.numRegs : 128;
+  cache[reinterpret_cast<const void*>(fn)] = r;
+  return r;
+}
+
+Plan plan_resident(const DevGraph& g, int64_t frames, bool early_stop) {
   Plan p;
   const size_t limit = static_cast<size_t>(device_smem_optin()) - 1024;
   const size_t per = frame_bytes(g);
   const size_t list_bytes = g.per_frame ? 2ull * g.list_slots : 0;  // per frame
   auto bytes = [&](int f) { return f * (per + list_bytes) + 20 * f + 16 * g.G + 32; };
+  const int bucket0 = cn_bucket(g.max_cdeg, g.cregular);
+  auto fv_for = [&](int fpc) {
+    const int fv = g_tune_fv.load();
+    if (fv > 0) return fv;
+    return (fpc >= 2 && fpc % 2 == 0 && bucket0 <= 8 && !g.per_frame) ? 2 : 1;
+  };
+  auto max_threads = [&](int fv) { return fv == 2 ? 256 : (bucket0 <= 8 ? 512 : (bucket0 <= 16 ? 256 : 128)); };
+  // one CN item per frame vector for the largest group, in whole warps where
+  // that stays a multiple of the frame vectors per CTA
+  auto threads_for = [&](int fpc, int fv) {
+    const int ng = fpc / fv;
+    int nt = (ng * g.max_cn_items + 31) / 32 * 32;
+    nt = std::max(64, std::min(nt, max_threads(fv)));
+    return nt / ng * ng;
+  };
   int fpc = g_tune_fpc.load();
   if (fpc <= 0) {
-    // largest FPC that still lets four CTAs share an SM (their barriers and
-    // latencies overlap; measured best on the C1 code), relaxing to two, then
-    // to whatever fits
-    const size_t sm_bytes = static_cast<size_t>(device_smem_per_sm()) - 4096;
-    fpc = 0;
-    for (int ctas : {4, 2, 1}) {
-      for (int c = g.per_frame ? 4 : 8; c >= 1 && fpc == 0; c /= 2)
-        if (bytes(c) <= limit && static_cast<size_t>(ctas) * bytes(c) <= sm_bytes) fpc = c;
-      if (fpc) break;
+    // the candidate with the most useful CN lanes per SM: resident CTAs
+    // (shared memory and registers) x frames per CTA x the fraction of the
+    // CTA's threads that hold a CN item of the largest group
+    const size_t sm_bytes = static_cast<size_t>(device_smem_per_sm());
+    double best = 0.0;
+    for (int c : {1, 2, 4, 8, 16}) {
+      if (bytes(c) > limit) continue;
+      // with early stop a CTA runs until its slowest frame converges: more
+      // than two frames per CTA idle their stopped lanes (measured slower)
+      if (early_stop && c > 2) continue;
+      if (g.per_frame && c > 4) continue;
+      const int fv = fv_for(c);
+      int bk = 0;
+      const KernelFn fn = pick_kernel(g, c, fv, &bk);
+      if (!fn) continue;
+      const int nt = threads_for(c, fv);
+      const int ng = c / fv;
+      const int regs = (kernel_regs(fn) * 32 + 255) / 256 * 256;  // per warp, allocation granularity
+      const int warps = (nt + 31) / 32;
+      const int by_regs = 65536 / (regs * warps);
+      const int by_smem = static_cast<int>(sm_bytes / (bytes(c) + 1024));
+      const int ctas = std::min({by_regs, by_smem, 32});
+      if (ctas <= 0) continue;
+      const double util = std::min(1.0, static_cast<double>(ng) * g.max_cn_items / (32.0 * warps));
+      const double score = ctas * c * util * (fv == 2 ? 2.0 : 1.0);  // two frames per instruction
+      if (score > best * 1.0001) {
+        best = score;
+        fpc = c;
+      }
     }
-    if (fpc == 0) fpc = 1;
+    if (fpc <= 0) fpc = 1;
   }
   if (bytes(fpc) > limit) return p;  // does not fit: no resident plan
   int bucket = 0;
-  int fv = g_tune_fv.load();
-  if (fv <= 0) fv = (fpc >= 2 && cn_bucket(g.max_cdeg, g.cregular) <= 8 && !g.per_frame) ? 2 : 1;
+  const int fv = fv_for(fpc);
   if (!pick_kernel(g, fpc, fv, &bucket)) return p;
-  const int max_nt = fv == 2 ? 256 : (bucket <= 8 ? 512 : (bucket <= 16 ? 256 : 128));
   const int ng = fpc / fv;  // frame vectors per CTA
   int nt = g_tune_threads.load();
-  if (nt <= 0) {
-    // one CN item per frame vector for the largest group, in whole warps
-    nt = (ng * g.max_cn_items + 31) / 32 * 32;
-    nt = std::max(64, std::min(nt, max_nt));
-  }
-  if (nt % ng || nt > max_nt) return p;
+  if (nt <= 0) nt = threads_for(fpc, fv);
+  if (nt % ng || nt > max_threads(fv)) return p;
   p.kernel = 1;
   p.fpc = fpc;
   p.fv = fv;
@@ -870,7 +926,7 @@ Plan plan_resident(const DevGraph& g, int64_t frames) {
 int launch_decode(const DevGraph& g, const DecodeArgs& a_in, void* stream, Plan* used) {
   DecodeArgs a = a_in;
   a.lazy_totals = g_lazy_totals.load();
-  const Plan p = plan_decode(g, a.frames);
+  const Plan p = plan_decode(g, a.frames, a.early_stop != 0);
   if (p.kernel == 2) return launch_stream(g, a, stream, used);
   if (used) *used = p;
   if (p.kernel == 0) return static_cast<int>(cudaErrorInvalidConfiguration);

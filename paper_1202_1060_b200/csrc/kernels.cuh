@@ -78,7 +78,9 @@ struct Plan {
   int64_t ctas = 0;
 };
 
-Plan plan_decode(const DevGraph& g, int64_t frames);
+// early_stop: the decode stops frames at a zero syndrome (changes the
+// preferred frames per CTA); plan queries without a decode use false
+Plan plan_decode(const DevGraph& g, int64_t frames, bool early_stop = false);
 // returns cudaError_t as int
 // per-frame group lists (gen_groups_kernel): out[(f * n_lists + l) * list_slots + j]
 // = slot j of the ordered groups of frame frame0+f at iteration list0+l+1
