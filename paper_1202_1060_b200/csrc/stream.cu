@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -39,13 +40,46 @@ struct ChunkState {
   int* berr = nullptr;    // [B]
 };
 
-__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
-__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
-__device__ __forceinline__ float& lane(float4& v, int i) { return reinterpret_cast<float*>(&v)[i]; }
-
-__device__ __forceinline__ bool quad_done(const ChunkState& s, int64_t q) {
-  const int4 d = *reinterpret_cast<const int4*>(s.done + 4 * q);
-  return d.x & d.y & d.z & d.w;
+// V consecutive frames per thread: one V*4-byte vector access per element
+template <int V>
+struct Vec {
+  float v[V];
+};
+template <int V>
+__device__ __forceinline__ Vec<V> ldv(const float* p) {
+  Vec<V> r;
+  if constexpr (V == 4) {
+    const float4 t = *reinterpret_cast<const float4*>(p);
+    r.v[0] = t.x, r.v[1] = t.y, r.v[2] = t.z, r.v[3] = t.w;
+  } else if constexpr (V == 2) {
+    const float2 t = *reinterpret_cast<const float2*>(p);
+    r.v[0] = t.x, r.v[1] = t.y;
+  } else {
+    r.v[0] = *p;
+  }
+  return r;
+}
+template <int V>
+__device__ __forceinline__ void stv(float* p, const Vec<V>& x) {
+  if constexpr (V == 4)
+    *reinterpret_cast<float4*>(p) = make_float4(x.v[0], x.v[1], x.v[2], x.v[3]);
+  else if constexpr (V == 2)
+    *reinterpret_cast<float2*>(p) = make_float2(x.v[0], x.v[1]);
+  else
+    *p = x.v[0];
+}
+// done flags of the thread's V frames, bit i = frame i
+template <int V>
+__device__ __forceinline__ unsigned done_bits(const ChunkState& s, int64_t q) {
+  if constexpr (V == 4) {
+    const int4 d = *reinterpret_cast<const int4*>(s.done + 4 * q);
+    return (d.x != 0) | (d.y != 0) << 1 | (d.z != 0) << 2 | (d.w != 0) << 3;
+  } else if constexpr (V == 2) {
+    const int2 d = *reinterpret_cast<const int2*>(s.done + 2 * q);
+    return (d.x != 0) | (d.y != 0) << 1;
+  } else {
+    return s.done[q] != 0;
+  }
 }
 
 // L = P = clamp(llr) in log2 units, transposed [nb][n] -> [n][B] through a
@@ -79,78 +113,77 @@ __global__ void stream_init(int n, const int32_t* __restrict__ pos, const float*
   }
 }
 
-// CN phase of one group over (record, quad) items.
-template <int D, bool EXACT>
+// CN phase of one group over (record, V-frame vector) items.
+template <int D, bool EXACT, int V>
 __global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ recs, int CS, int count, ChunkState s) {
-  const int64_t QB = s.B / 4;
+  const int64_t QB = s.B / V;
   const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (item >= count * QB) return;
   const int j = static_cast<int>(item / QB);
   const int64_t q = item - j * QB;
-  const int4 dn = *reinterpret_cast<const int4*>(s.done + 4 * q);
-  if (dn.x & dn.y & dn.z & dn.w) return;
+  const unsigned dn = done_bits<V>(s, q);
+  if (dn == (1u << V) - 1) return;
   const CnRecord<D, EXACT> cr(recs + static_cast<int64_t>(j) * CS, CS);
   const int base = cr.slot();
   const unsigned mask = cr.mask();
   const int deg = cr.deg();
-  float4 pv[D], old[D];
+  Vec<V> pv[D], old[D];
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     if (cr.has(k)) {
-      pv[k] = ld4(s.P + static_cast<int64_t>(cr.var(k)) * s.B + 4 * q);
-      old[k] = ld4(s.c2v + static_cast<int64_t>(base + k) * s.B + 4 * q);
+      pv[k] = ldv<V>(s.P + static_cast<int64_t>(cr.var(k)) * s.B + V * q);
+      old[k] = ldv<V>(s.c2v + static_cast<int64_t>(base + k) * s.B + V * q);
     } else {
-      pv[k] = old[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < V; ++i) pv[k].v[i] = old[k].v[i] = 0.f;
     }
   }
-  float4 out[D];
+  Vec<V> out[D];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < V; ++i) {
     float x[D];
 #pragma unroll
-    for (int k = 0; k < D; ++k) x[k] = lane(pv[k], i) - lane(old[k], i);
-    boxplus_row<D, EXACT>(x, deg, [&](int k, float c) { lane(out[k], i) = c; });
+    for (int k = 0; k < D; ++k) x[k] = pv[k].v[i] - old[k].v[i];
+    boxplus_row<D, EXACT>(x, deg, [&](int k, float c) { out[k].v[i] = c; });
   }
   // frames that already stopped (decoder.hpp:173-177) keep their state
-  const int dl[4] = {dn.x, dn.y, dn.z, dn.w};
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-    if (dl[i])
+  for (int i = 0; i < V; ++i)
+    if (dn & (1u << i))
 #pragma unroll
-      for (int k = 0; k < D; ++k) lane(out[k], i) = lane(old[k], i);
+      for (int k = 0; k < D; ++k) out[k].v[i] = old[k].v[i];
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     if (!cr.has(k)) continue;
-    st4(s.c2v + static_cast<int64_t>(base + k) * s.B + 4 * q, out[k]);
+    stv<V>(s.c2v + static_cast<int64_t>(base + k) * s.B + V * q, out[k]);
     if (mask & (1u << k)) {
-      float4 p = pv[k];
+      Vec<V> p;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) lane(p, i) = (lane(pv[k], i) - lane(old[k], i)) + lane(out[k], i);
-      st4(s.P + static_cast<int64_t>(cr.var(k)) * s.B + 4 * q, p);
+      for (int i = 0; i < V; ++i) p.v[i] = (pv[k].v[i] - old[k].v[i]) + out[k].v[i];
+      stv<V>(s.P + static_cast<int64_t>(cr.var(k)) * s.B + V * q, p);
     }
   }
 }
 
 // P_v = L_v + sum of c2v over the VN's edges, ascending CN order (the totals
-// of decoder.hpp:162-165), over (VN record, quad) items.
+// of decoder.hpp:162-165), over (VN record, V-frame vector) items.
+template <int V>
 __global__ void __launch_bounds__(256) stream_vnsum(const int4* __restrict__ recs, int vs4, int count, ChunkState s,
                                                     int skip_done) {
-  const int64_t QB = s.B / 4;
+  const int64_t QB = s.B / V;
   const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (item >= count * QB) return;
   const int j = static_cast<int>(item / QB);
   const int64_t q = item - j * QB;
-  if (skip_done && quad_done(s, q)) return;
+  if (skip_done && done_bits<V>(s, q) == (1u << V) - 1) return;
   const int4* rec = recs + static_cast<int64_t>(j) * vs4;
   int4 t = __ldg(rec);
   const int v = t.x;
-  float4 acc = ld4(s.L + static_cast<int64_t>(v) * s.B + 4 * q);
+  Vec<V> acc = ldv<V>(s.L + static_cast<int64_t>(v) * s.B + V * q);
   auto add = [&](int slot) {
-    const float4 c = ld4(s.c2v + static_cast<int64_t>(slot) * s.B + 4 * q);
-    acc.x += c.x;
-    acc.y += c.y;
-    acc.z += c.z;
-    acc.w += c.w;
+    const Vec<V> c = ldv<V>(s.c2v + static_cast<int64_t>(slot) * s.B + V * q);
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc.v[i] += c.v[i];
   };
   add(t.y);
   add(t.z);
@@ -162,30 +195,30 @@ __global__ void __launch_bounds__(256) stream_vnsum(const int4* __restrict__ rec
     add(t.z);
     add(t.w);
   }
-  st4(s.P + static_cast<int64_t>(v) * s.B + 4 * q, acc);
+  stv<V>(s.P + static_cast<int64_t>(v) * s.B + V * q, acc);
 }
 
-// Syndrome weight per frame (decoder.hpp:129-137) over (CN, quad) items.
-template <int D, bool EXACT>
+// Syndrome weight per frame (decoder.hpp:129-137) over (CN, V-frame vector) items.
+template <int D, bool EXACT, int V>
 __global__ void __launch_bounds__(256) stream_syndrome(const int32_t* __restrict__ recs, int CS, int m, ChunkState s) {
-  const int64_t QB = s.B / 4;
+  const int64_t QB = s.B / V;
   const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (item >= m * QB) return;
   const int r = static_cast<int>(item / QB);
   const int64_t q = item - r * QB;
-  if (quad_done(s, q)) return;
+  if (done_bits<V>(s, q) == (1u << V) - 1) return;
   const CnRecord<D, EXACT> cr(recs + static_cast<int64_t>(r) * CS, CS);
   unsigned p = 0;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     if (!cr.has(k)) continue;
-    const float4 v = ld4(s.P + static_cast<int64_t>(cr.var(k)) * s.B + 4 * q);
-    p ^= static_cast<unsigned>(v.x < 0.f) | static_cast<unsigned>(v.y < 0.f) << 1 |
-         static_cast<unsigned>(v.z < 0.f) << 2 | static_cast<unsigned>(v.w < 0.f) << 3;
+    const Vec<V> x = ldv<V>(s.P + static_cast<int64_t>(cr.var(k)) * s.B + V * q);
+#pragma unroll
+    for (int i = 0; i < V; ++i) p ^= static_cast<unsigned>(x.v[i] < 0.f) << i;
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-    if (p & (1u << i)) atomicAdd(s.weight + 4 * q + i, 1);
+  for (int i = 0; i < V; ++i)
+    if (p & (1u << i)) atomicAdd(s.weight + V * q + i, 1);
 }
 
 // Per-frame bookkeeping after a syndrome test (decoder.hpp:170-177).
@@ -295,15 +328,33 @@ __global__ void stream_dump(const DevGraph g, ChunkState s, float* c2v_out, floa
 struct StreamKernels {
   void (*cn)(const int32_t*, int, int, ChunkState);
   void (*syn)(const int32_t*, int, int, ChunkState);
+  void (*vnsum)(const int4*, int, int, ChunkState, int);
 };
 
-StreamKernels pick(const DevGraph& g) {
+template <int V>
+StreamKernels pick_v(const DevGraph& g) {
   switch (cn_bucket(g.max_cdeg, g.cregular)) {
-    case 3: return {stream_cn<3, true>, stream_syndrome<3, true>};
-    case 6: return {stream_cn<6, true>, stream_syndrome<6, true>};
-    case 8: return {stream_cn<8, false>, stream_syndrome<8, false>};
-    case 16: return {stream_cn<16, false>, stream_syndrome<16, false>};
-    default: return {nullptr, nullptr};
+    case 3: return {stream_cn<3, true, V>, stream_syndrome<3, true, V>, stream_vnsum<V>};
+    case 6: return {stream_cn<6, true, V>, stream_syndrome<6, true, V>, stream_vnsum<V>};
+    case 8: return {stream_cn<8, false, V>, stream_syndrome<8, false, V>, stream_vnsum<V>};
+    case 16: return {stream_cn<16, false, V>, stream_syndrome<16, false, V>, stream_vnsum<V>};
+    default: return {nullptr, nullptr, nullptr};
+  }
+}
+
+// frames per thread: 4 by default (16-byte accesses); LDPCB_STREAM_V = 1 / 2
+// (A/B: more threads per launch for small chunks)
+int stream_lanes() {
+  const char* e = std::getenv("LDPCB_STREAM_V");
+  const int v = e ? std::atoi(e) : 4;
+  return (v == 1 || v == 2) ? v : 4;
+}
+
+StreamKernels pick(const DevGraph& g) {
+  switch (stream_lanes()) {
+    case 1: return pick_v<1>(g);
+    case 2: return pick_v<2>(g);
+    default: return pick_v<4>(g);
   }
 }
 
@@ -323,6 +374,7 @@ Plan plan_stream(const DevGraph& g, int64_t frames) {
   const size_t budget = std::min<size_t>(free_b / 3, 24ull << 30);
   int64_t B = static_cast<int64_t>(budget / chunk_bytes_per_frame(g)) / 128 * 128;
   B = std::min<int64_t>(B, 16384);
+  if (const char* e = std::getenv("LDPCB_STREAM_CHUNK")) B = std::min<int64_t>(B, std::max(4, std::atoi(e)) / 4 * 4);
   const int64_t need = (std::max<int64_t>(frames, 1) + 3) / 4 * 4;
   B = std::min(B, need);
   if (B < 4) return p;
@@ -335,12 +387,10 @@ Plan plan_stream(const DevGraph& g, int64_t frames) {
   return p;
 }
 
-int launch_stream(const DevGraph& g, const DecodeArgs& a, void* stream_v, Plan* used) {
-  const Plan p = plan_stream(g, a.frames);
-  if (used) *used = p;
-  if (p.kernel == 0) return static_cast<int>(cudaErrorInvalidConfiguration);
-  if (a.frames <= 0) return 0;
-  auto st = static_cast<cudaStream_t>(stream_v);
+namespace {
+
+// One sequence of chunks on one stream.
+int launch_stream_one(const DevGraph& g, const DecodeArgs& a, cudaStream_t st, const Plan& p) {
   const StreamKernels K = pick(g);
   const int64_t B = p.fpc;
   ChunkState s;
@@ -358,7 +408,7 @@ int launch_stream(const DevGraph& g, const DecodeArgs& a, void* stream_v, Plan* 
   s.conv = s.iters + B;
   s.berr = s.conv + B;
   const int tpb = 256;
-  const int64_t QB = B / 4;
+  const int64_t QB = B / stream_lanes();
   const bool dump = a.max_subiters > 0;
   int launches = 0;
   for (int64_t f0 = 0; f0 < a.frames && err == cudaSuccess; f0 += B) {
@@ -388,7 +438,7 @@ int launch_stream(const DevGraph& g, const DecodeArgs& a, void* stream_v, Plan* 
         }
         const int x0 = g.h_fix_off[grp], xn = g.h_fix_off[grp + 1] - x0;
         if (xn > 0) {
-          stream_vnsum<<<blocks_for(xn * QB, tpb), tpb, 0, st>>>(
+          K.vnsum<<<blocks_for(xn * QB, tpb), tpb, 0, st>>>(
               reinterpret_cast<const int4*>(g.fix_rec) + static_cast<size_t>(x0) * g.vs4, g.vs4, xn, s, 1);
           ++launches;
         }
@@ -396,8 +446,8 @@ int launch_stream(const DevGraph& g, const DecodeArgs& a, void* stream_v, Plan* 
       if (stop || dump) continue;
       const bool check = a.early_stop || a.trace || iter == a.max_iters;
       if (g.recompute && (check || !a.lazy_totals)) {
-        stream_vnsum<<<blocks_for(g.n * QB, tpb), tpb, 0, st>>>(reinterpret_cast<const int4*>(g.all_vn_rec), g.vs4,
-                                                                g.n, s, 1);
+        K.vnsum<<<blocks_for(g.n * QB, tpb), tpb, 0, st>>>(reinterpret_cast<const int4*>(g.all_vn_rec), g.vs4, g.n,
+                                                           s, 1);
         ++launches;
       }
       if (!check) continue;
@@ -407,8 +457,8 @@ int launch_stream(const DevGraph& g, const DecodeArgs& a, void* stream_v, Plan* 
     }
     if (dump) {
       if (g.recompute)
-        stream_vnsum<<<blocks_for(g.n * QB, tpb), tpb, 0, st>>>(reinterpret_cast<const int4*>(g.all_vn_rec),
-                                                                g.vs4, g.n, s, 0);
+        K.vnsum<<<blocks_for(g.n * QB, tpb), tpb, 0, st>>>(reinterpret_cast<const int4*>(g.all_vn_rec), g.vs4, g.n,
+                                                           s, 0);
       stream_dump<<<blocks_for(static_cast<int64_t>(g.E) * s.nb, tpb), tpb, 0, st>>>(g, s, a.c2v_out, a.v2c_out,
                                                                                       f0);
       launches += 2;
@@ -424,6 +474,16 @@ int launch_stream(const DevGraph& g, const DecodeArgs& a, void* stream_v, Plan* 
   note_launches(launches);
   cudaFreeAsync(mem, st);
   return static_cast<int>(err);
+}
+
+}  // namespace
+
+int launch_stream(const DevGraph& g, const DecodeArgs& a, void* stream_v, Plan* used) {
+  const Plan p = plan_stream(g, a.frames);
+  if (used) *used = p;
+  if (p.kernel == 0) return static_cast<int>(cudaErrorInvalidConfiguration);
+  if (a.frames <= 0) return 0;
+  return launch_stream_one(g, a, static_cast<cudaStream_t>(stream_v), p);
 }
 
 }  // namespace ldpcb

@@ -1,0 +1,13 @@
+#!/bin/bash
+# Full ncu capture of one decode_resident launch (C5 n=1008 workload at 65536
+# frames) and its text summaries (metrics, source-level stall hot spots).
+mkdir -p gpurun_out
+SMALL="python bench.py --frames 65536 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e ${SMALL_ARGS}"
+$SMALL > gpurun_out/small.log 2>&1 || { cat gpurun_out/small.log; exit 1; }
+ncu --set full --clock-control none --import-source on -k regex:decode_resident -s 1 -c 1 -f -o gpurun_out/prof_res $SMALL > gpurun_out/ncu_full.log 2>&1
+tail -2 gpurun_out/ncu_full.log
+ncu -i gpurun_out/prof_res.ncu-rep --page source --csv --print-source sass > gpurun_out/prof_res_sass.csv 2>/dev/null
+ncu -i gpurun_out/prof_res.ncu-rep --page raw --csv > gpurun_out/prof_res_raw.csv 2>/dev/null
+ncu -i gpurun_out/prof_res.ncu-rep --page details --csv > gpurun_out/prof_res_details.csv 2>/dev/null
+python scripts/ncu_hot.py gpurun_out/prof_res_sass.csv 60 > gpurun_out/prof_res_hot.txt 2>&1
+ls -la gpurun_out
