@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -647,17 +648,20 @@ __global__ void check_update_kernel(int deg, int64_t rows, const float* __restri
 // needed. next_below's two 64-bit remainders use per-CTA reciprocals.
 struct Below {
   const unsigned long long* recip;  // recip[n] = floor((2^64-1) / n)
-  __device__ __forceinline__ uint64_t mod(uint64_t x, uint32_t n) const {
-    uint64_t r = x - __umul64hi(x, recip[n]) * n;  // quotient low by at most 2
-    while (r >= n) r -= n;
-    return r;
+  // x mod n for n < 2^16: the Barrett quotient is low by at most 2, so the
+  // remainder is < 3n < 2^32 and only the low words of x - q n are needed
+  __device__ __forceinline__ uint32_t mod(uint64_t x, uint32_t n) const {
+    uint32_t r = static_cast<uint32_t>(x) - static_cast<uint32_t>(__umul64hi(x, recip[n])) * n;
+    r = r >= n ? r - n : r;
+    return r >= n ? r - n : r;
   }
   // Stream::below (rng.hpp:67-73): rejection below lim = (2^64 - n) mod n,
   // which is < n <= 65535, so it is only computed for such tiny draws
   __device__ __forceinline__ uint32_t draw(Stream& rng, uint32_t n) const {
     for (;;) {
       const uint64_t x = rng.u64();
-      if (x > 0xffffull || x >= mod(0ull - n, n)) return static_cast<uint32_t>(mod(x, n));
+      if (x > 0xffffull) return mod(x, n);
+      if (x >= mod(0ull - n, n)) return mod(x, n);
     }
   }
   __device__ __forceinline__ void permute(Stream& rng, uint16_t* a, int n) const {  // rng.hpp:75-82
@@ -676,9 +680,8 @@ __global__ void gen_groups_kernel(int M, int G, int balanced, int nominal, int k
   extern __shared__ unsigned long long gsm64[];
   unsigned long long* recip = gsm64;  // [M + 1]
   for (int i = threadIdx.x; i <= M; i += blockDim.x) recip[i] = i > 1 ? ~0ull / static_cast<unsigned>(i) : 0ull;
-  const int per = (M + nominal) | 1;  // uint16 per thread (odd: spread banks)
+  const int per = M | 1;  // uint16 per thread (odd: spread banks)
   uint16_t* pool = reinterpret_cast<uint16_t*>(gsm64 + M + 1) + threadIdx.x * per;
-  uint16_t* cand = pool + M;
   __syncthreads();
   const Below bl{recip};
   const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -698,7 +701,8 @@ __global__ void gen_groups_kernel(int M, int G, int balanced, int nominal, int k
   for (int i = 0; i < next; ++i) o[i] = pool[i];
   int fresh_start = 0, fresh_len = next;  // fresh part of the previous group
   for (int grp = 1; grp < G; ++grp) {
-    for (int i = 0; i < fresh_len; ++i) cand[i] = pool[fresh_start + i];
+    // the candidates are permuted in place: that pool range is never read again
+    uint16_t* cand = pool + fresh_start;
     bl.permute(rng, cand, fresh_len);
     const int take = min(k, fresh_len);
     for (int i = 0; i < take; ++i) o[w++] = cand[i];
@@ -810,12 +814,20 @@ int launch_gen_groups(const DevGraph& g, int64_t frame0, int64_t frames, int lis
                       void* stream) {
   if (!g.per_frame) return static_cast<int>(cudaErrorInvalidValue);
   if (frames <= 0 || n_lists <= 0) return 0;
-  const int per = 2 * ((g.m + g.nominal) | 1);  // scratch bytes per thread
-  const int fixed = 8 * (g.m + 1);                // reciprocal table
+  const int per = 2 * (g.m | 1);    // scratch bytes per thread (the pool)
+  const int fixed = 8 * (g.m + 1);  // reciprocal table
   const int room = device_smem_optin() - 1024 - fixed;
   if (per > room) return static_cast<int>(cudaErrorInvalidConfiguration);
-  // 128 lists per CTA where they fit (about 1.3 KB each for M = 504)
-  const int tpb = std::max(1, std::min(128, room / per));
+  // one list per thread: the most lists resident per SM (each is a
+  // latency-bound sequential shuffle), the larger CTA on ties
+  int tpb = 1, best = 0;
+  for (int t : {32, 64, 96, 128, 192, 256}) {
+    if (t * per > room) break;
+    const int lists = t * (device_smem_per_sm() / (fixed + t * per + 1024));
+    if (lists >= best) best = lists, tpb = t;
+  }
+  if (best == 0) tpb = std::max(1, std::min(128, room / per));
+  if (const char* e = std::getenv("LDPCB_GEN_TPB")) tpb = std::max(1, std::min(room / per, std::atoi(e)));
   const int bytes = fixed + tpb * per;
   cudaError_t err = cudaFuncSetAttribute(reinterpret_cast<const void*>(gen_groups_kernel),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
