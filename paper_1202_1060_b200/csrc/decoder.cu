@@ -384,17 +384,54 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
       if constexpr (RND) {
         const int c0 = s_go[grp].x, cn = s_go[grp].y - c0;
         const uint16_t* lst = s_list + fb * slots + c0;
-        if (live)
-          for (int j = j0; j < cn; j += jstep)
+        // the thread's first CN record was requested one group ahead (group 0:
+        // now, after the iteration's lists were staged); the next group's now
+        Rec cur = next_cn;
+        if (grp == 0 && j0 < cn) cur.load(g.all_rec + lst[j0] * CS, CS);
+        if (grp + 1 < g.G) {
+          const int c1 = s_go[grp + 1].x;
+          if (j0 < s_go[grp + 1].y - c1) next_cn.load(g.all_rec + s_list[fb * slots + c1 + j0] * CS, CS);
+        }
+        if (live && j0 < cn) {
+          cn_update<D, EXACT, FPC, FV, true>(c2v, P, cur, live);
+          for (int j = j0 + jstep; j < cn; j += jstep)
             cn_update<D, EXACT, FPC, FV, true>(c2v, P, Rec(g.all_rec + lst[j] * CS, CS), live);
+        }
+        // VN records of the first CN's edges, requested before the barrier
+        constexpr int KT = D <= 8 ? D : 1;
+        int4 t0[KT];
+        if constexpr (D <= 8)
+          if (live && j0 < cn)
+#pragma unroll
+            for (int k = 0; k < D; ++k)
+              if (cur.has(k)) t0[k] = __ldg(all_vn + cur.var(k) * vs4);
         __syncthreads();
         // every VN of the group re-summed from its record (a VN shared by
-        // several CNs is written several times with the same value)
-        if (live)
-          for (int e = j0; e < cn * D; e += jstep) {
-            const int v = Rec(g.all_rec + lst[e / D] * CS, CS).var(e % D);
-            if (EXACT || v >= 0) vn_sum<FPC, FV, VS>(c2v, P, L, all_vn + v * vs4, vs4, __ldg(all_vn + v * vs4));
+        // several CNs is written several times with the same value): each
+        // thread re-sums the VNs of the CNs it updated, their VN records
+        // requested before any is used
+        auto resum = [&](const Rec& r) {
+#pragma unroll
+          for (int k0 = 0; k0 < D; k0 += 4) {
+            int4 t[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (k0 + u < D && r.has(k0 + u)) t[u] = __ldg(all_vn + r.var(k0 + u) * vs4);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (k0 + u < D && r.has(k0 + u)) vn_sum<FPC, FV, VS>(c2v, P, L, all_vn + r.var(k0 + u) * vs4, vs4, t[u]);
           }
+        };
+        if (live && j0 < cn) {
+          if constexpr (D <= 8) {
+#pragma unroll
+            for (int k = 0; k < D; ++k)
+              if (cur.has(k)) vn_sum<FPC, FV, VS>(c2v, P, L, all_vn + cur.var(k) * vs4, vs4, t0[k]);
+          } else {
+            resum(cur);
+          }
+          for (int j = j0 + jstep; j < cn; j += jstep) resum(Rec(g.all_rec + lst[j] * CS, CS));
+        }
         __syncthreads();
         continue;
       }
