@@ -339,9 +339,23 @@ def run_b200(args):
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e_dt = float(te.item())
+        # the host link alone: a bare pinned host -> device copy of the same LLR bytes
+        d_tmp = torch.empty_like(llr[:Be])
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d_tmp.copy_(h_llr, non_blocking=True)
+        c0.record(stream)
+        for _ in range(3):
+            d_tmp.copy_(h_llr, non_blocking=True)
+        c1.record(stream)
+        torch.cuda.synchronize()
+        link_gbs = 3 * Be * n * 4 / (c0.elapsed_time(c1) / 1e3) / 1e9
+        del d_tmp
         e2e = {"value": Be * e_steps * world * K / e_dt, "unit": UNIT, "h2d_bytes_per_step": Be * n * 4,
                "d2h_bytes_per_step": Be * ((n + 7) // 8) + 48,
-               "api": "ldpcb_decode_host (pinned host LLRs in, packed bits + counters out)"}
+               "api": "ldpcb_decode_host (pinned host LLRs in, packed bits + counters out)",
+               "h2d_gbs": round(Be * n * 4 * e_steps / e_dt / 1e9, 2),
+               "h2d_link_gbs": round(link_gbs, 2),
+               "note": "h2d_gbs = LLR bytes / e2e step time; h2d_link_gbs = a bare pinned copy of the same bytes"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
