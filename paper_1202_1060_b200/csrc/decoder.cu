@@ -114,14 +114,27 @@ __device__ __forceinline__ void cn_update(float* __restrict__ c2v, float* __rest
     // one frame: v2c in registers only; every output is stored as the
     // boxplus emits it (keeps wide rows, D = 16 / 32, within the register file)
     if (!ALL_LIVE && !(live & 1u)) return;
-    float x[D];
+    auto row = [&](auto width) {
+      constexpr int W = decltype(width)::value;
+      float x[W];
 #pragma unroll
-    for (int k = 0; k < D; ++k) x[k] = cr.has(k) ? P[cr.var(k) * FPC] - c2v[(base + k) * FPC] : 0.f;
-    boxplus_row<D, EXACT>(x, deg, [&](int k, float c) {
-      c2v[(base + k) * FPC] = c;
-      // in-place posterior: P + (c - old) = v2c + c (v2c = P - old, unclamped)
-      if (mask & (1u << k)) P[cr.var(k) * FPC] = x[k] + c;
-    });
+      for (int k = 0; k < W; ++k) x[k] = cr.has(k) ? P[cr.var(k) * FPC] - c2v[(base + k) * FPC] : 0.f;
+      boxplus_row<W, EXACT && W == D>(x, deg, [&](int k, float c) {
+        c2v[(base + k) * FPC] = c;
+        // in-place posterior: P + (c - old) = v2c + c (v2c = P - old, unclamped)
+        if (mask & (1u << k)) P[cr.var(k) * FPC] = x[k] + c;
+      });
+    };
+    // wide buckets: rows of degree <= 8 (most QC block rows; warps are
+    // homogeneous because a group lists whole block rows) take the 8-wide
+    // code, whose predicated-off positions no longer cost issue slots
+    if constexpr (!EXACT && D > 8) {
+      if (deg <= 8) {
+        row(std::integral_constant<int, 8>{});
+        return;
+      }
+    }
+    row(std::integral_constant<int, D>{});
     return;
   }
   FVec<FV> pv[D], old[D], out[D];
