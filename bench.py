@@ -313,8 +313,8 @@ def run_b200(args):
                             f"{s.edge_updates_per_iter} CN-edge updates + {HBM_BYTES_PER_TOUCH} B x "
                             f"{s.touched_per_iter} touched VNs) + LLR in + bits out, x {B} frames / CUDA-event time "
                             f"{kernel_ms:.3f} ms; peak = MEASURED_PEAKS hbm_gbs; traffic = ncu DRAM bytes of all "
-                            "stream kernels per frame (profiles/dram_bytes_per_frame.json) x frames: below the "
-                            "algorithmic bytes because part of each group's working set is served from L2"}
+                            "stream kernels per frame (profiles/dram_bytes_per_frame.json, one 8192-frame decode) "
+                            "x frames: 1.05x the algorithmic bytes (syndrome, init and bit-packing passes)"}
 
     # ---- end to end through the host C-ABI call (pinned host buffers)
     e2e = None
