@@ -624,6 +624,238 @@ finish:
 #endif
 }
 
+// ---- early-stop decoding from a frame queue (persistent CTAs)
+// With early stop a CTA of the kernel above runs until its slowest frame
+// stops, and every CTA pays its own prologue. Here a persistent CTA keeps FPC
+// frame slots busy: at an iteration boundary (where every frame is at group
+// 0 of the same cyclic schedule) a slot whose frame stopped writes that
+// frame's outputs and takes the next frame id from a global counter. Each
+// frame's arithmetic is the same as in decode_resident (slots are
+// independent lanes), so outputs are bit-identical; frames finish in any
+// order.
+template <int D, bool EXACT, int FPC, int FV, int VS>
+__global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decode_queue(const DevGraph g,
+                                                                                       const DecodeArgs a,
+                                                                                       unsigned long long* queue) {
+  const int CS = g.cs;
+  constexpr int NG = FPC / FV;
+  extern __shared__ __align__(16) float smem[];
+  __shared__ int s_active, s_retiring;
+  __shared__ long long s_frame[FPC];
+  __shared__ unsigned long long s_cnt[6];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int n = g.n, m = g.m, S = g.n_slots;
+  const int vs4 = VS > 0 ? VS : g.vs4;
+  const int fg = tid % NG, j0 = tid / NG, jstep = nt / NG;
+  const int fb = fg * FV;
+  float* const c2v = smem + fb;
+  float* const P = smem + S * FPC + fb;
+  float* const L = P + n * FPC;
+  float* const P0 = smem + S * FPC;  // slot-indexed views
+  float* const L0 = P0 + n * FPC;
+  int* const s_done = reinterpret_cast<int*>(smem + (S + 2 * n) * FPC);
+  int* const s_weight = s_done + FPC;
+  int* const s_iters = s_weight + FPC;
+  int* const s_conv = s_iters + FPC;
+  int* const s_berr = s_conv + FPC;
+  int4* const s_go = reinterpret_cast<int4*>(smem + (((S + 2 * n) * FPC + 5 * FPC + 3) & ~3));
+  const int4* const tot_vn = reinterpret_cast<const int4*>(g.tot_vn_rec);
+  const int4* const fix_vn = reinterpret_cast<const int4*>(g.fix_rec);
+  const int nb = (n + 7) >> 3;
+
+  // init_state (decoder.hpp:39-52) of slot ff for frame f (f < 0: idle slot)
+  auto load_slot = [&](int ff, long long f) {
+    if (f >= 0) {
+      const float* llr = a.llr + f * n;
+      if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(a.llr) & 15) == 0) {
+        const float4* l4 = reinterpret_cast<const float4*>(llr);
+        for (int b = tid; b < n / 4; b += nt) {
+          const float4 x = __ldg(l4 + b);
+          const float r[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int v = __ldg(g.vn_pos + 4 * b + u);
+            const float y = clamp_llr(r[u]) * kLog2e;
+            P0[v * FPC + ff] = y;
+            L0[v * FPC + ff] = y;
+          }
+        }
+      } else {
+        for (int i = tid; i < n; i += nt) {
+          const int v = __ldg(g.vn_pos + i);
+          const float y = clamp_llr(__ldg(llr + i)) * kLog2e;
+          P0[v * FPC + ff] = y;
+          L0[v * FPC + ff] = y;
+        }
+      }
+      if (a.trace)
+        for (int i = tid; i < a.max_iters; i += nt) a.trace[f * a.max_iters + i] = -1;
+    } else {
+      for (int i = tid; i < n; i += nt) P0[i * FPC + ff] = L0[i * FPC + ff] = kClampB;
+    }
+    for (int i = tid; i < S; i += nt) smem[i * FPC + ff] = 0.f;
+  };
+  auto pull = [&]() -> long long {
+    const unsigned long long f = atomicAdd(queue, 1ull);
+    return f < static_cast<unsigned long long>(a.frames) ? static_cast<long long>(f) : -1ll;
+  };
+
+  if (tid < FPC) {
+    s_frame[tid] = pull();
+    s_done[tid] = s_frame[tid] < 0;
+    s_weight[tid] = s_iters[tid] = s_conv[tid] = s_berr[tid] = 0;
+  }
+  if (tid < 6) s_cnt[tid] = 0ull;
+  for (int i = tid; i < g.G; i += nt)
+    s_go[i] = make_int4(__ldg(g.cn_off + i), __ldg(g.cn_off + i + 1), __ldg(g.fix_off + i), __ldg(g.fix_off + i + 1));
+  __syncthreads();
+  for (int ff = 0; ff < FPC; ++ff) load_slot(ff, s_frame[ff]);
+  __syncthreads();
+  auto live_bits = [&]() {
+    unsigned b = 0;
+#pragma unroll
+    for (int i = 0; i < FV; ++i) b |= static_cast<unsigned>(!s_done[fb + i]) << i;
+    return b;
+  };
+  unsigned live = live_bits();
+  using Rec = ResidentRecord<D, EXACT>;
+  Rec next_cn;
+  if (j0 < s_go[0].y - s_go[0].x) next_cn.load(g.cn_rec + static_cast<size_t>(s_go[0].x + j0) * CS, CS);
+  int4 go = s_go[0];
+
+  for (;;) {
+    // one iteration for every busy slot (decoder.hpp:157-160), as in decode_resident
+    for (int grp = 0; grp < g.G; ++grp) {
+      const int c0 = go.x, cn = go.y - go.x;
+      const int x0 = go.z, xn = go.w - go.z;
+      const int4 ngo = s_go[grp + 1 < g.G ? grp + 1 : 0];
+      int4 fix_first = make_int4(0, 0, 0, 0);
+      if (j0 < xn) fix_first = __ldg(fix_vn + static_cast<size_t>(x0 + j0) * vs4);
+      const Rec cur = next_cn;
+      if (j0 < ngo.y - ngo.x) next_cn.load(g.cn_rec + static_cast<size_t>(ngo.x + j0) * CS, CS);
+      if (live && j0 < cn) {
+        const int32_t* rec = g.cn_rec + static_cast<size_t>(c0) * CS;
+        if (live == (1u << FV) - 1) {
+          cn_update<D, EXACT, FPC, FV, true>(c2v, P, cur, live);
+          for (int j = j0 + jstep; j < cn; j += jstep)
+            cn_update<D, EXACT, FPC, FV, true>(c2v, P, Rec(rec + j * CS, CS), live);
+        } else {
+          cn_update<D, EXACT, FPC, FV, false>(c2v, P, cur, live);
+          for (int j = j0 + jstep; j < cn; j += jstep)
+            cn_update<D, EXACT, FPC, FV, false>(c2v, P, Rec(rec + j * CS, CS), live);
+        }
+      }
+      __syncthreads();
+      pin(fix_first);
+      if (xn > 0) {
+        if (live && j0 < xn) {
+          const int4* rec = fix_vn + static_cast<size_t>(x0) * vs4;
+          vn_sum<FPC, FV, VS>(c2v, P, L, rec + j0 * vs4, vs4, fix_first);
+          vn_sum_range<FPC, FV, VS>(c2v, P, L, rec, vs4, j0 + jstep, xn, jstep);
+        }
+        __syncthreads();
+      }
+      pin_rec(next_cn);
+      go = ngo;
+    }
+    // exact totals, hard decisions, syndrome weights (decoder.hpp:162-171)
+    if (g.recompute) {
+      if (live) vn_sum_range<FPC, FV, VS>(c2v, P, L, tot_vn, vs4, j0, n, jstep);
+      __syncthreads();
+    }
+    if (live) {
+      int w[FV] = {};
+      for (int j = j0; j < m; j += jstep) {
+        const unsigned p = parity<D, EXACT, FPC, FV>(P, g.all_rec + j * CS, CS);
+#pragma unroll
+        for (int i = 0; i < FV; ++i) w[i] += (p >> i) & 1u;
+      }
+#pragma unroll
+      for (int i = 0; i < FV; ++i)
+        if (w[i]) atomicAdd(&s_weight[fb + i], w[i]);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int retiring = 0;
+      for (int ff = 0; ff < FPC; ++ff) {
+        if (s_done[ff]) continue;
+        const int w = s_weight[ff], it = ++s_iters[ff];
+        s_weight[ff] = 0;
+        if (a.trace) a.trace[s_frame[ff] * a.max_iters + it - 1] = w;
+        s_conv[ff] = w == 0;
+        if ((w == 0 && a.early_stop) || it == a.max_iters) {  // decoder.hpp:173-177
+          s_done[ff] = 2;                                       // retiring
+          ++retiring;
+        }
+      }
+      s_retiring = retiring;
+    }
+    __syncthreads();
+    if (s_retiring == 0) continue;
+    // outputs of the frames that stopped (sim.hpp:119-123), then refill
+    for (int ff = 0; ff < FPC; ++ff) {
+      if (s_done[ff] != 2) continue;
+      const long long f = s_frame[ff];
+      int errs = 0;
+      if (a.bits && a.bits_packed) {
+        for (int b = tid; b < nb; b += nt) {
+          unsigned byte = 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int v = b * 8 + j;
+            if (v < n && P0[__ldg(g.vn_pos + v) * FPC + ff] < 0.f) byte |= 1u << j;
+          }
+          a.bits[f * nb + b] = static_cast<uint8_t>(byte);
+          errs += __popc(byte);
+        }
+      } else if (a.bits || a.counters || a.bit_errors) {
+        for (int v = tid; v < n; v += nt) {
+          const int bit = P0[__ldg(g.vn_pos + v) * FPC + ff] < 0.f;
+          if (a.bits) a.bits[f * n + v] = static_cast<uint8_t>(bit);
+          errs += bit;
+        }
+      }
+      if (errs) atomicAdd(&s_berr[ff], errs);
+      if (a.posterior)
+        for (int v = tid; v < n; v += nt) a.posterior[f * n + v] = P0[__ldg(g.vn_pos + v) * FPC + ff] * kLn2;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int ff = 0; ff < FPC; ++ff) {
+        if (s_done[ff] != 2) continue;
+        const long long f = s_frame[ff];
+        const int it = s_iters[ff];
+        if (a.iterations) a.iterations[f] = it;
+        if (a.converged) a.converged[f] = static_cast<uint8_t>(s_conv[ff]);
+        if (a.bit_errors) a.bit_errors[f] = s_berr[ff];
+        s_cnt[0] += 1;
+        s_cnt[1] += s_berr[ff];
+        s_cnt[2] += s_berr[ff] > 0;
+        s_cnt[3] += s_conv[ff];
+        s_cnt[4] += it;
+        s_cnt[5] += s_conv[ff] ? it : 0;
+        s_frame[ff] = pull();
+        s_done[ff] = s_frame[ff] < 0 ? 1 : 3;  // 3: refilled this round
+        s_iters[ff] = s_conv[ff] = s_berr[ff] = 0;
+      }
+      int active = 0;
+      for (int ff = 0; ff < FPC; ++ff) active += s_done[ff] != 1;
+      s_active = active;
+    }
+    __syncthreads();
+    for (int ff = 0; ff < FPC; ++ff)
+      if (s_done[ff] == 3) load_slot(ff, s_frame[ff]);
+    __syncthreads();
+    if (tid < FPC && s_done[tid] == 3) s_done[tid] = 0;
+    __syncthreads();
+    live = live_bits();
+    if (s_active == 0) break;
+  }
+  if (tid == 0 && a.counters)
+    for (int i = 0; i < 6; ++i)
+      if (s_cnt[i]) atomicAdd(a.counters + i, s_cnt[i]);
+}
+
 // ---- channel: transmit_all_zero (channel.hpp:38-46), fp64 then fp32
 __global__ void channel_kernel(int n, double sigma, double scale, uint64_t seed, int64_t frame0, int64_t frames,
                                float* __restrict__ llr) {
@@ -788,6 +1020,34 @@ KernelFn pick_fpc(int fpc, int fv) {
   }
 }
 
+using QueueFn = void (*)(const DevGraph, const DecodeArgs, unsigned long long*);
+
+// frame-queue kernels for the early-stop plans (frames per CTA <= 2)
+template <int D, bool EXACT, int VS>
+QueueFn pick_queue_fpc(int fpc, int fv) {
+  if constexpr (D <= 8) {
+    if (fv == 2) return fpc == 2 ? decode_queue<D, EXACT, 2, 2, VS> : nullptr;
+  }
+  if (fv != 1) return nullptr;
+  switch (fpc) {
+    case 1: return decode_queue<D, EXACT, 1, 1, VS>;
+    case 2: return decode_queue<D, EXACT, 2, 1, VS>;
+    default: return nullptr;
+  }
+}
+
+QueueFn pick_queue(const DevGraph& g, int fpc, int fv) {
+  if (g.per_frame) return nullptr;
+  switch (cn_bucket(g.max_cdeg, g.cregular)) {
+    case 6: return g.vs4 == 1 ? pick_queue_fpc<6, true, 1>(fpc, fv) : pick_queue_fpc<6, true, 0>(fpc, fv);
+    case 3: return pick_queue_fpc<3, true, 0>(fpc, fv);
+    case 8: return pick_queue_fpc<8, false, 0>(fpc, fv);
+    case 16: return pick_queue_fpc<16, false, 0>(fpc, fv);
+    case 32: return pick_queue_fpc<32, false, 0>(fpc, fv);
+    default: return nullptr;
+  }
+}
+
 template <int D, bool EXACT, int VS>
 KernelFn pick_rnd(int fpc) {
   switch (fpc) {
@@ -856,6 +1116,14 @@ void note_launches(int n) { g_launches += n; }
 void set_force_kernel(int kernel) { g_force_kernel = kernel; }
 
 void set_lazy_totals(int on) { g_lazy_totals = on; }
+
+// early-stop decodes from a frame queue (decode_queue) when the batch holds
+// at least four waves of CTAs; LDPCB_FRAME_QUEUE=0 never, =2 for any batch
+// (A/B and tests)
+static int frame_queue_mode() {
+  const char* e = std::getenv("LDPCB_FRAME_QUEUE");
+  return e ? std::atoi(e) : 1;
+}
 int lazy_totals() { return g_lazy_totals.load(); }
 
 Plan plan_resident(const DevGraph& g, int64_t frames, bool early_stop);
@@ -999,6 +1267,28 @@ int launch_decode(const DevGraph& g, const DecodeArgs& a_in, void* stream, Plan*
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem);
   if (err != cudaSuccess) return static_cast<int>(err);
   auto st = static_cast<cudaStream_t>(stream);
+  if (!g.per_frame && a.early_stop && a.max_subiters == 0 && frame_queue_mode() > 0) {
+    // early stop: persistent CTAs take frames from a queue (decode_queue)
+    const QueueFn qf = pick_queue(g, p.fpc, p.fv);
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    if (qf && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+        cudaFuncSetAttribute(reinterpret_cast<const void*>(qf), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             p.smem) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qf, p.threads, p.smem) == cudaSuccess &&
+        per_sm > 0 && (p.ctas >= 4ll * sms * per_sm || frame_queue_mode() == 2)) {
+      unsigned long long* queue = nullptr;
+      err = cudaMallocAsync(reinterpret_cast<void**>(&queue), sizeof(unsigned long long), st);
+      if (err == cudaSuccess) err = cudaMemsetAsync(queue, 0, sizeof(unsigned long long), st);
+      if (err != cudaSuccess) return static_cast<int>(err);
+      qf<<<static_cast<unsigned>(std::min<int64_t>(p.ctas, static_cast<int64_t>(sms) * per_sm)), p.threads, p.smem, st>>>(
+          g, a, queue);
+      ++g_launches;
+      err = cudaGetLastError();
+      cudaFreeAsync(queue, st);
+      return static_cast<int>(err);
+    }
+  }
   if (!g.per_frame) {
     // grid.x limit is 2^31-1, far above any batch
     fn<<<static_cast<unsigned>(p.ctas), p.threads, p.smem, st>>>(g, a);

@@ -457,3 +457,33 @@ def test_c4_long_code_parity(P, torch, orc):
               f"posteriors within 1e-3 {frac:.6f} (max {worst:.2e})")
         assert same.mean() >= (1.0 if not es else 0.95)
         assert frac >= 0.9999
+
+
+@pytest.mark.parametrize("case", ["c1_nd", "c1_gs", "c1_bp", "irregular", "c3_nd"])
+def test_frame_queue_is_bit_identical(P, torch, orc, case):
+    """Early stop from a frame queue (persistent CTAs refill a slot when its
+    frame stops) against one frame set per CTA: every output identical,
+    counters included, frames finishing in any order."""
+    if case.startswith("c1"):
+        g = P.configs.c1_code()
+        s = P.configs.c1_schedules(g)[{"c1_nd": "ndgsbp", "c1_gs": "gsbp", "c1_bp": "bp"}[case]]
+    elif case == "c3_nd":
+        g = P.configs.c3_code()
+        s = P.configs.c3_schedules(g)["ndgsbp"]
+    else:
+        g = P.TannerGraph.irregular(2400, [2, 3, 8], [1200, 960, 240], 6, 5)
+        s = P.GroupSchedule.windows(g, 5, 300, 240)
+    llr = cu(torch, orc.transmit_batch_f32(P.sigma2_from_ebn0(1.75, g.rate), 3, g.n_vars, 0, 3001, THREADS))
+    outs = {}
+    try:
+        for mode in ("0", "2"):
+            os.environ["LDPCB_FRAME_QUEUE"] = mode
+            cnt = torch.zeros(6, dtype=torch.int64, device="cuda")
+            r = to_np(P.decode_batch(g, s, llr, 20, posterior=True, trace=True, counters=cnt))
+            r["counters"] = cnt.cpu().numpy()
+            r["packed"] = to_np(P.decode_batch(g, s, llr, 20, packed=True))["bits"]
+            outs[mode] = r
+    finally:
+        os.environ.pop("LDPCB_FRAME_QUEUE", None)
+    for k in outs["0"]:
+        assert np.array_equal(outs["0"][k], outs["2"][k]), k
