@@ -250,6 +250,67 @@ __device__ __forceinline__ unsigned parity(const float* __restrict__ P, const in
   return p;
 }
 
+// One sub-iteration of a per-frame grouping (RND): group grp of the frame's
+// staged list `lst` (decoder.hpp:112-127). CN phase from the per-CN records,
+// barrier, then every VN of the group re-summed exactly, barrier. The
+// thread's first CN record was requested one group ahead (group 0: now,
+// after the iteration's lists were staged); the next group's is requested here.
+template <int D, bool EXACT, int FPC, int FV, int VS, class Rec>
+__device__ __forceinline__ void rnd_group(const DevGraph& g, int CS, int vs4, float* __restrict__ c2v,
+                                          float* __restrict__ P, const float* __restrict__ L, const int4* s_go,
+                                          const uint16_t* lst0, int grp, int j0, int jstep, unsigned live,
+                                          Rec& next_cn) {
+  const int4* const all_vn = reinterpret_cast<const int4*>(g.all_vn_rec);  // indexed by VN position
+  const int c0 = s_go[grp].x, cn = s_go[grp].y - c0;
+  const uint16_t* lst = lst0 + c0;
+  Rec cur = next_cn;
+  if (grp == 0 && j0 < cn) cur.load(g.all_rec + lst[j0] * CS, CS);
+  if (grp + 1 < g.G) {
+    const int c1 = s_go[grp + 1].x;
+    if (j0 < s_go[grp + 1].y - c1) next_cn.load(g.all_rec + lst0[c1 + j0] * CS, CS);
+  }
+  if (live && j0 < cn) {
+    cn_update<D, EXACT, FPC, FV, true>(c2v, P, cur, live);
+    for (int j = j0 + jstep; j < cn; j += jstep)
+      cn_update<D, EXACT, FPC, FV, true>(c2v, P, Rec(g.all_rec + lst[j] * CS, CS), live);
+  }
+  // VN records of the first CN's edges, requested before the barrier
+  constexpr int KT = D <= 8 ? D : 1;
+  int4 t0[KT];
+  if constexpr (D <= 8)
+    if (live && j0 < cn)
+#pragma unroll
+      for (int k = 0; k < D; ++k)
+        if (cur.has(k)) t0[k] = __ldg(all_vn + cur.var(k) * vs4);
+  __syncthreads();
+  // every VN of the group re-summed from its record (a VN shared by several
+  // CNs is written several times with the same value): each thread re-sums
+  // the VNs of the CNs it updated, their VN records requested before any is used
+  auto resum = [&](const Rec& r) {
+#pragma unroll
+    for (int k0 = 0; k0 < D; k0 += 4) {
+      int4 t[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (k0 + u < D && r.has(k0 + u)) t[u] = __ldg(all_vn + r.var(k0 + u) * vs4);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (k0 + u < D && r.has(k0 + u)) vn_sum<FPC, FV, VS>(c2v, P, L, all_vn + r.var(k0 + u) * vs4, vs4, t[u]);
+    }
+  };
+  if (live && j0 < cn) {
+    if constexpr (D <= 8) {
+#pragma unroll
+      for (int k = 0; k < D; ++k)
+        if (cur.has(k)) vn_sum<FPC, FV, VS>(c2v, P, L, all_vn + cur.var(k) * vs4, vs4, t0[k]);
+    } else {
+      resum(cur);
+    }
+    for (int j = j0 + jstep; j < cn; j += jstep) resum(Rec(g.all_rec + lst[j] * CS, CS));
+  }
+  __syncthreads();
+}
+
 constexpr int max_threads_for(int D, int FV) { return FV == 2 ? 256 : (D <= 8 ? 512 : (D <= 16 ? 256 : 128)); }
 
 #ifdef LDPCB_PHASE_TIMING
@@ -291,7 +352,6 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
   int4* const s_go = reinterpret_cast<int4*>(smem + (((S + 2 * n) * FPC + 5 * FPC + 3) & ~3));
   uint16_t* const s_list = reinterpret_cast<uint16_t*>(s_go + g.G);  // RND: [FPC][slots]
   const int slots = a.list_slots;
-  const int4* const all_vn = reinterpret_cast<const int4*>(g.all_vn_rec);  // indexed by VN (RND)
   const int4* const tot_vn = reinterpret_cast<const int4*>(g.tot_vn_rec);  // bank-coloured order
   const int4* const fix_vn = reinterpret_cast<const int4*>(g.fix_rec);
 
@@ -383,9 +443,11 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
     if constexpr (RND) {
       if (iter == 1 || a.n_lists > 1) {  // this iteration's groups (decoder.hpp:153-156)
         const int li = a.n_lists > 1 ? iter - 1 : 0;
-        for (int i = tid; i < nf * slots; i += nt) {
+        // padding frames get CN 0 everywhere: their record loads (issued
+        // whether or not the frame is live) must stay in bounds
+        for (int i = tid; i < FPC * slots; i += nt) {
           const int ff = i / slots, j = i - ff * slots;
-          s_list[ff * slots + j] = a.lists[((f0 + ff) * a.n_lists + li) * slots + j];
+          s_list[i] = ff < nf ? a.lists[((f0 + ff) * a.n_lists + li) * slots + j] : 0;
         }
         __syncthreads();
       }
@@ -395,57 +457,8 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
       ++sub;
       // CN phase: every (CN of the group, frame vector); Jacobi within the group
       if constexpr (RND) {
-        const int c0 = s_go[grp].x, cn = s_go[grp].y - c0;
-        const uint16_t* lst = s_list + fb * slots + c0;
-        // the thread's first CN record was requested one group ahead (group 0:
-        // now, after the iteration's lists were staged); the next group's now
-        Rec cur = next_cn;
-        if (grp == 0 && j0 < cn) cur.load(g.all_rec + lst[j0] * CS, CS);
-        if (grp + 1 < g.G) {
-          const int c1 = s_go[grp + 1].x;
-          if (j0 < s_go[grp + 1].y - c1) next_cn.load(g.all_rec + s_list[fb * slots + c1 + j0] * CS, CS);
-        }
-        if (live && j0 < cn) {
-          cn_update<D, EXACT, FPC, FV, true>(c2v, P, cur, live);
-          for (int j = j0 + jstep; j < cn; j += jstep)
-            cn_update<D, EXACT, FPC, FV, true>(c2v, P, Rec(g.all_rec + lst[j] * CS, CS), live);
-        }
-        // VN records of the first CN's edges, requested before the barrier
-        constexpr int KT = D <= 8 ? D : 1;
-        int4 t0[KT];
-        if constexpr (D <= 8)
-          if (live && j0 < cn)
-#pragma unroll
-            for (int k = 0; k < D; ++k)
-              if (cur.has(k)) t0[k] = __ldg(all_vn + cur.var(k) * vs4);
-        __syncthreads();
-        // every VN of the group re-summed from its record (a VN shared by
-        // several CNs is written several times with the same value): each
-        // thread re-sums the VNs of the CNs it updated, their VN records
-        // requested before any is used
-        auto resum = [&](const Rec& r) {
-#pragma unroll
-          for (int k0 = 0; k0 < D; k0 += 4) {
-            int4 t[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              if (k0 + u < D && r.has(k0 + u)) t[u] = __ldg(all_vn + r.var(k0 + u) * vs4);
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              if (k0 + u < D && r.has(k0 + u)) vn_sum<FPC, FV, VS>(c2v, P, L, all_vn + r.var(k0 + u) * vs4, vs4, t[u]);
-          }
-        };
-        if (live && j0 < cn) {
-          if constexpr (D <= 8) {
-#pragma unroll
-            for (int k = 0; k < D; ++k)
-              if (cur.has(k)) vn_sum<FPC, FV, VS>(c2v, P, L, all_vn + cur.var(k) * vs4, vs4, t0[k]);
-          } else {
-            resum(cur);
-          }
-          for (int j = j0 + jstep; j < cn; j += jstep) resum(Rec(g.all_rec + lst[j] * CS, CS));
-        }
-        __syncthreads();
+        rnd_group<D, EXACT, FPC, FV, VS>(g, CS, vs4, c2v, P, L, s_go, s_list + fb * slots, grp, j0, jstep, live,
+                                         next_cn);
         continue;
       }
       PT_MARK(pt_a);
@@ -633,10 +646,13 @@ finish:
 // frame's arithmetic is the same as in decode_resident (slots are
 // independent lanes), so outputs are bit-identical; frames finish in any
 // order.
-template <int D, bool EXACT, int FPC, int FV, int VS>
+// RND: per-frame groupings, each slot staging its own frame's list for the
+// slot's own iteration (lists indexed by the frame's id, as in decode_resident).
+template <int D, bool EXACT, int FPC, int FV, int VS, bool RND = false>
 __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decode_queue(const DevGraph g,
                                                                                        const DecodeArgs a,
                                                                                        unsigned long long* queue) {
+  static_assert(!RND || FV == 1, "per-frame groupings need one frame per thread");
   const int CS = g.cs;
   constexpr int NG = FPC / FV;
   extern __shared__ __align__(16) float smem[];
@@ -659,6 +675,8 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
   int* const s_conv = s_iters + FPC;
   int* const s_berr = s_conv + FPC;
   int4* const s_go = reinterpret_cast<int4*>(smem + (((S + 2 * n) * FPC + 5 * FPC + 3) & ~3));
+  uint16_t* const s_list = reinterpret_cast<uint16_t*>(s_go + g.G);  // RND: [FPC][slots]
+  const int slots = a.list_slots;
   const int4* const tot_vn = reinterpret_cast<const int4*>(g.tot_vn_rec);
   const int4* const fix_vn = reinterpret_cast<const int4*>(g.fix_rec);
   const int nb = (n + 7) >> 3;
@@ -720,12 +738,30 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
   unsigned live = live_bits();
   using Rec = ResidentRecord<D, EXACT>;
   Rec next_cn;
-  if (j0 < s_go[0].y - s_go[0].x) next_cn.load(g.cn_rec + static_cast<size_t>(s_go[0].x + j0) * CS, CS);
+  if (!RND && j0 < s_go[0].y - s_go[0].x) next_cn.load(g.cn_rec + static_cast<size_t>(s_go[0].x + j0) * CS, CS);
   int4 go = s_go[0];
 
   for (;;) {
+    if constexpr (RND) {
+      // each busy slot's groups for its own next iteration (decoder.hpp:153-156)
+      for (int i = tid; i < FPC * slots; i += nt) {
+        const int ff = i / slots;
+        if (s_done[ff]) {  // idle slot: CN 0 keeps its (unused) record loads in bounds
+          s_list[i] = 0;
+          continue;
+        }
+        const int li = a.n_lists > 1 ? s_iters[ff] : 0;
+        s_list[i] = a.lists[(s_frame[ff] * a.n_lists + li) * slots + (i - ff * slots)];
+      }
+      __syncthreads();
+    }
     // one iteration for every busy slot (decoder.hpp:157-160), as in decode_resident
     for (int grp = 0; grp < g.G; ++grp) {
+      if constexpr (RND) {
+        rnd_group<D, EXACT, FPC, FV, VS>(g, CS, vs4, c2v, P, L, s_go, s_list + fb * slots, grp, j0, jstep, live,
+                                         next_cn);
+        continue;
+      }
       const int c0 = go.x, cn = go.y - go.x;
       const int x0 = go.z, xn = go.w - go.z;
       const int4 ngo = s_go[grp + 1 < g.G ? grp + 1 : 0];
@@ -759,7 +795,7 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
       go = ngo;
     }
     // exact totals, hard decisions, syndrome weights (decoder.hpp:162-171)
-    if (g.recompute) {
+    if (!RND && g.recompute) {
       if (live) vn_sum_range<FPC, FV, VS>(c2v, P, L, tot_vn, vs4, j0, n, jstep);
       __syncthreads();
     }
@@ -1036,8 +1072,26 @@ QueueFn pick_queue_fpc(int fpc, int fv) {
   }
 }
 
+template <int D, bool EXACT, int VS>
+QueueFn pick_queue_rnd(int fpc) {
+  switch (fpc) {
+    case 1: return decode_queue<D, EXACT, 1, 1, VS, true>;
+    case 2: return decode_queue<D, EXACT, 2, 1, VS, true>;
+    default: return nullptr;
+  }
+}
+
 QueueFn pick_queue(const DevGraph& g, int fpc, int fv) {
-  if (g.per_frame) return nullptr;
+  if (g.per_frame) {
+    if (fv != 1) return nullptr;
+    switch (cn_bucket(g.max_cdeg, g.cregular)) {
+      case 6: return g.vs4 == 1 ? pick_queue_rnd<6, true, 1>(fpc) : pick_queue_rnd<6, true, 0>(fpc);
+      case 3: return pick_queue_rnd<3, true, 0>(fpc);
+      case 8: return pick_queue_rnd<8, false, 0>(fpc);
+      case 16: return pick_queue_rnd<16, false, 0>(fpc);
+      default: return nullptr;
+    }
+  }
   switch (cn_bucket(g.max_cdeg, g.cregular)) {
     case 6: return g.vs4 == 1 ? pick_queue_fpc<6, true, 1>(fpc, fv) : pick_queue_fpc<6, true, 0>(fpc, fv);
     case 3: return pick_queue_fpc<3, true, 0>(fpc, fv);
@@ -1234,6 +1288,10 @@ Plan plan_resident(const DevGraph& g, int64_t frames, bool early_stop) {
       }
     }
     if (fpc <= 0) fpc = 1;
+    // per-frame groupings with early stop: two frames per CTA taken from the
+    // frame queue beat one frame per CTA at more CTAs per SM (C1, G = 8,
+    // r = 0.25, <= 20 it: 6.68e6 -> 7.38e6 frames/s; regrouping 3.02e6 -> 3.14e6)
+    if (g.per_frame && early_stop && frame_queue_mode() > 0 && fpc == 1 && bytes(2) <= limit) fpc = 2;
   }
   if (bytes(fpc) > limit) return p;  // does not fit: no resident plan
   int bucket = 0;
@@ -1267,28 +1325,34 @@ int launch_decode(const DevGraph& g, const DecodeArgs& a_in, void* stream, Plan*
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem);
   if (err != cudaSuccess) return static_cast<int>(err);
   auto st = static_cast<cudaStream_t>(stream);
-  if (!g.per_frame && a.early_stop && a.max_subiters == 0 && frame_queue_mode() > 0) {
-    // early stop: persistent CTAs take frames from a queue (decode_queue)
-    const QueueFn qf = pick_queue(g, p.fpc, p.fv);
+  // early stop: persistent CTAs take frames from a queue (decode_queue) when
+  // the batch (or a per-frame chunk) is at least four waves
+  QueueFn qf = nullptr;
+  int64_t resident = 0;  // CTAs resident on the device
+  if (a.early_stop && a.max_subiters == 0 && frame_queue_mode() > 0) {
+    qf = pick_queue(g, p.fpc, p.fv);
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
-    if (qf && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+    if (!qf || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
         cudaFuncSetAttribute(reinterpret_cast<const void*>(qf), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             p.smem) == cudaSuccess &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qf, p.threads, p.smem) == cudaSuccess &&
-        per_sm > 0 && (p.ctas >= 4ll * sms * per_sm || frame_queue_mode() == 2)) {
-      unsigned long long* queue = nullptr;
-      err = cudaMallocAsync(reinterpret_cast<void**>(&queue), sizeof(unsigned long long), st);
-      if (err == cudaSuccess) err = cudaMemsetAsync(queue, 0, sizeof(unsigned long long), st);
-      if (err != cudaSuccess) return static_cast<int>(err);
-      qf<<<static_cast<unsigned>(std::min<int64_t>(p.ctas, static_cast<int64_t>(sms) * per_sm)), p.threads, p.smem, st>>>(
-          g, a, queue);
-      ++g_launches;
-      err = cudaGetLastError();
-      cudaFreeAsync(queue, st);
-      return static_cast<int>(err);
-    }
+                             p.smem) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qf, p.threads, p.smem) != cudaSuccess || per_sm <= 0)
+      qf = nullptr;
+    resident = static_cast<int64_t>(sms) * per_sm;
   }
+  auto use_queue = [&](int64_t ctas) { return qf && (ctas >= 4 * resident || frame_queue_mode() == 2); };
+  auto launch_queue = [&](const DecodeArgs& b, int64_t ctas) {
+    unsigned long long* queue = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&queue), sizeof(unsigned long long), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(queue, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    qf<<<static_cast<unsigned>(std::min(ctas, resident)), p.threads, p.smem, st>>>(g, b, queue);
+    ++g_launches;
+    e = cudaGetLastError();
+    cudaFreeAsync(queue, st);
+    return e;
+  };
+  if (!g.per_frame && use_queue(p.ctas)) return static_cast<int>(launch_queue(a, p.ctas));
   if (!g.per_frame) {
     // grid.x limit is 2^31-1, far above any batch
     fn<<<static_cast<unsigned>(p.ctas), p.threads, p.smem, st>>>(g, a);
@@ -1323,7 +1387,12 @@ int launch_decode(const DevGraph& g, const DecodeArgs& a_in, void* stream, Plan*
     b.lists = lists;
     err = static_cast<cudaError_t>(launch_gen_groups(g, b.frame0, cnt, 0, a.n_lists, lists, st));
     if (err != cudaSuccess) break;
-    fn<<<static_cast<unsigned>((cnt + p.fpc - 1) / p.fpc), p.threads, p.smem, st>>>(g, b);
+    const int64_t ctas = (cnt + p.fpc - 1) / p.fpc;
+    if (use_queue(ctas)) {
+      err = launch_queue(b, ctas);
+      continue;
+    }
+    fn<<<static_cast<unsigned>(ctas), p.threads, p.smem, st>>>(g, b);
     ++g_launches;
     err = cudaGetLastError();
   }

@@ -30,6 +30,7 @@ using namespace dev;
 struct ChunkState {
   int64_t B = 0;     // layout stride (frames), multiple of 4
   int nb = 0;        // frames of this chunk that are real
+  int zero_slot = 0; // the always-zero c2v slot that pads VN records
   float* c2v = nullptr;
   float* P = nullptr;
   float* L = nullptr;
@@ -167,6 +168,8 @@ __global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ rec
 
 // P_v = L_v + sum of c2v over the VN's edges, ascending CN order (the totals
 // of decoder.hpp:162-165), over (VN record, V-frame vector) items.
+// Records are padded with the zero slot after the VN's last edge; the loop
+// stops there (a warp serves one VN, so the exit is warp-uniform).
 template <int V>
 __global__ void __launch_bounds__(256) stream_vnsum(const int4* __restrict__ recs, int vs4, int count, ChunkState s,
                                                     int skip_done) {
@@ -185,15 +188,19 @@ __global__ void __launch_bounds__(256) stream_vnsum(const int4* __restrict__ rec
 #pragma unroll
     for (int i = 0; i < V; ++i) acc.v[i] += c.v[i];
   };
-  add(t.y);
-  add(t.z);
-  add(t.w);
-  for (int r = 1; r < vs4; ++r) {
+  const int zero = s.zero_slot;
+  auto add_nz = [&](int slot) {
+    if (slot != zero) add(slot);
+  };
+  add_nz(t.y);
+  add_nz(t.z);
+  add_nz(t.w);
+  for (int r = 1; r < vs4 && t.w != zero; ++r) {
     t = __ldg(rec + r);
-    add(t.x);
-    add(t.y);
-    add(t.z);
-    add(t.w);
+    add_nz(t.x);
+    add_nz(t.y);
+    add_nz(t.z);
+    add_nz(t.w);
   }
   stv<V>(s.P + static_cast<int64_t>(v) * s.B + V * q, acc);
 }
@@ -395,6 +402,7 @@ int launch_stream_one(const DevGraph& g, const DecodeArgs& a, cudaStream_t st, c
   const int64_t B = p.fpc;
   ChunkState s;
   s.B = B;
+  s.zero_slot = g.n_slots - 1;
   const size_t state_bytes = 4ull * (static_cast<size_t>(g.n_slots) + 2ull * g.n) * B;
   char* mem = nullptr;
   cudaError_t err = cudaMallocAsync(reinterpret_cast<void**>(&mem), state_bytes + 5 * 4 * B + 256, st);

@@ -101,3 +101,27 @@ def test_per_frame_simulate_counters_and_frame_ids(P, torch, corc):
     assert whole[0] == ref[0]
     assert abs(int(whole[2]) - int(ref[2])) <= 4 + 0.002 * ref[0]
     assert abs(int(whole[4]) - int(ref[4])) <= 0.002 * ref[4] + 20
+
+
+@pytest.mark.parametrize("regroup,code", [(True, "c1"), (False, "c1"), (True, "c3")])
+def test_per_frame_frame_queue_is_bit_identical(P, torch, regroup, code):
+    """Early stop from a frame queue with per-frame groupings: a refilled slot
+    stages its own frame's list for its own iteration, so every output
+    (counters included) equals one frame set per CTA."""
+    g = P.configs.c1_code() if code == "c1" else P.configs.c3_code()
+    s = P.GroupSchedule.per_frame(g, P.NONDISJOINT, 8 if code == "c1" else 6, 0.25, 17, regroup)
+    llr = P.transmit_all_zero(g.n_vars, P.sigma2_from_ebn0(1.75, g.rate), 3, 0, 3001)
+    outs = {}
+    try:
+        for mode in ("0", "2"):
+            os.environ["LDPCB_FRAME_QUEUE"] = mode
+            cnt = torch.zeros(6, dtype=torch.int64, device="cuda")
+            r = to_np(P.decode_batch(g, s, llr, 20, posterior=True, trace=True, counters=cnt))
+            r["counters"] = cnt.cpu().numpy()
+            outs[mode] = r
+    finally:
+        os.environ.pop("LDPCB_FRAME_QUEUE", None)
+    for k in outs["0"]:
+        a, b = outs["0"][k], outs["2"][k]
+        bad = np.nonzero((a != b).reshape(len(a), -1).any(axis=1))[0] if a.ndim else []
+        assert np.array_equal(a, b), (k, bad[:8], len(bad))
