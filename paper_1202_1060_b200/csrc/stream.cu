@@ -41,6 +41,16 @@ struct ChunkState {
   int* berr = nullptr;    // [B]
 };
 
+// Programmatic dependent launch (per-group kernels): a CTA lets the next
+// kernel of the stream start launching at once, and waits for the previous
+// kernel to complete (and its writes to be visible) before touching state.
+// The next kernel's CTAs are placed as this kernel's last wave drains, which
+// hides the launch gap between ~900 dependent launches per chunk.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // V consecutive frames per thread: one V*4-byte vector access per element
 template <int V>
 struct Vec {
@@ -117,6 +127,7 @@ __global__ void stream_init(int n, const int32_t* __restrict__ pos, const float*
 // CN phase of one group over (record, V-frame vector) items.
 template <int D, bool EXACT, int V>
 __global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ recs, int CS, int count, ChunkState s) {
+  pdl_enter();
   const int64_t QB = s.B / V;
   const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (item >= count * QB) return;
@@ -173,6 +184,7 @@ __global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ rec
 template <int V>
 __global__ void __launch_bounds__(256) stream_vnsum(const int4* __restrict__ recs, int vs4, int count, ChunkState s,
                                                     int skip_done) {
+  pdl_enter();
   const int64_t QB = s.B / V;
   const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (item >= count * QB) return;
@@ -208,6 +220,7 @@ __global__ void __launch_bounds__(256) stream_vnsum(const int4* __restrict__ rec
 // Syndrome weight per frame (decoder.hpp:129-137) over (CN, V-frame vector) items.
 template <int D, bool EXACT, int V>
 __global__ void __launch_bounds__(256) stream_syndrome(const int32_t* __restrict__ recs, int CS, int m, ChunkState s) {
+  pdl_enter();
   const int64_t QB = s.B / V;
   const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (item >= m * QB) return;
@@ -231,6 +244,7 @@ __global__ void __launch_bounds__(256) stream_syndrome(const int32_t* __restrict
 // Per-frame bookkeeping after a syndrome test (decoder.hpp:170-177).
 __global__ void stream_iter_end(ChunkState s, int iter, int early_stop, int32_t* trace, int max_iters,
                                 int64_t frame0) {
+  pdl_enter();
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= s.nb || s.done[f]) return;
   const int w = s.weight[f];
@@ -371,6 +385,28 @@ size_t chunk_bytes_per_frame(const DevGraph& g) {
 
 unsigned blocks_for(int64_t items, int tpb) { return static_cast<unsigned>((items + tpb - 1) / tpb); }
 
+// LDPCB_STREAM_PDL=0 launches the per-group kernels without the programmatic
+// dependency attribute (A/B); griddepcontrol is then a no-op.
+bool stream_pdl() {
+  const char* e = std::getenv("LDPCB_STREAM_PDL");
+  return !e || std::atoi(e) != 0;
+}
+
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), unsigned blocks, int tpb, cudaStream_t st, bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(tpb);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 }  // namespace
 
 Plan plan_stream(const DevGraph& g, int64_t frames) {
@@ -418,6 +454,7 @@ int launch_stream_one(const DevGraph& g, const DecodeArgs& a, cudaStream_t st, c
   const int tpb = 256;
   const int64_t QB = B / stream_lanes();
   const bool dump = a.max_subiters > 0;
+  const bool pdl = stream_pdl();
   int launches = 0;
   for (int64_t f0 = 0; f0 < a.frames && err == cudaSuccess; f0 += B) {
     s.nb = static_cast<int>(std::min<int64_t>(B, a.frames - f0));
@@ -432,7 +469,7 @@ int launch_stream_one(const DevGraph& g, const DecodeArgs& a, cudaStream_t st, c
     }
     int sub = 0;
     bool stop = false;
-    for (int iter = 1; iter <= a.max_iters && !stop; ++iter) {
+    for (int iter = 1; iter <= a.max_iters && !stop && err == cudaSuccess; ++iter) {
       for (int grp = 0; grp < g.G; ++grp) {
         if (dump && sub == a.max_subiters) {
           stop = true;
@@ -441,26 +478,34 @@ int launch_stream_one(const DevGraph& g, const DecodeArgs& a, cudaStream_t st, c
         ++sub;
         const int c0 = g.h_cn_off[grp], cn = g.h_cn_off[grp + 1] - c0;
         if (cn > 0) {
-          K.cn<<<blocks_for(cn * QB, tpb), tpb, 0, st>>>(g.cn_rec + static_cast<size_t>(c0) * g.cs, g.cs, cn, s);
+          err = launch_pdl(K.cn, blocks_for(cn * QB, tpb), tpb, st, pdl, g.cn_rec + static_cast<size_t>(c0) * g.cs,
+                           g.cs, cn, s);
           ++launches;
         }
         const int x0 = g.h_fix_off[grp], xn = g.h_fix_off[grp + 1] - x0;
-        if (xn > 0) {
-          K.vnsum<<<blocks_for(xn * QB, tpb), tpb, 0, st>>>(
-              reinterpret_cast<const int4*>(g.fix_rec) + static_cast<size_t>(x0) * g.vs4, g.vs4, xn, s, 1);
+        if (xn > 0 && err == cudaSuccess) {
+          err = launch_pdl(K.vnsum, blocks_for(xn * QB, tpb), tpb, st, pdl,
+                           reinterpret_cast<const int4*>(g.fix_rec) + static_cast<size_t>(x0) * g.vs4, g.vs4, xn,
+                           s, 1);
           ++launches;
+        }
+        if (err != cudaSuccess) {
+          stop = true;
+          break;
         }
       }
       if (stop || dump) continue;
       const bool check = a.early_stop || a.trace || iter == a.max_iters;
       if (g.recompute && (check || !a.lazy_totals)) {
-        K.vnsum<<<blocks_for(g.n * QB, tpb), tpb, 0, st>>>(reinterpret_cast<const int4*>(g.all_vn_rec), g.vs4, g.n,
-                                                           s, 1);
+        err = launch_pdl(K.vnsum, blocks_for(g.n * QB, tpb), tpb, st, pdl,
+                         reinterpret_cast<const int4*>(g.all_vn_rec), g.vs4, g.n, s, 1);
         ++launches;
       }
-      if (!check) continue;
-      K.syn<<<blocks_for(g.m * QB, tpb), tpb, 0, st>>>(g.all_rec, g.cs, g.m, s);
-      stream_iter_end<<<blocks_for(s.nb, tpb), tpb, 0, st>>>(s, iter, a.early_stop, a.trace, a.max_iters, f0);
+      if (!check || err != cudaSuccess) continue;
+      err = launch_pdl(K.syn, blocks_for(g.m * QB, tpb), tpb, st, pdl, g.all_rec, g.cs, g.m, s);
+      if (err == cudaSuccess)
+        err = launch_pdl(stream_iter_end, blocks_for(s.nb, tpb), tpb, st, pdl, s, iter, a.early_stop, a.trace,
+                         a.max_iters, f0);
       launches += 2;
     }
     if (dump) {
@@ -477,7 +522,7 @@ int launch_stream_one(const DevGraph& g, const DecodeArgs& a, cudaStream_t st, c
       stream_final<<<blocks_for(s.nb, tpb), tpb, 0, st>>>(s, a, f0);
       launches += 2;
     }
-    err = cudaGetLastError();
+    if (err == cudaSuccess) err = cudaGetLastError();
   }
   note_launches(launches);
   cudaFreeAsync(mem, st);
