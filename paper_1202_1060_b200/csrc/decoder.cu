@@ -190,12 +190,17 @@ __device__ __forceinline__ void cn_update(float* __restrict__ c2v, float* __rest
 
 // P_v = L_v + sum of c2v over the VN's edges in ascending-CN order: the
 // totals of decoder.hpp:162-165 (and every v2c of v refreshed at once).
+// Records are padded with the zero slot after the VN's last edge: padding is
+// skipped and the record walk stops at the first row that ends in padding
+// (fix-up and totals records are grouped by VN degree, so warps stop together).
 template <int FPC, int FV, int VS>
 __device__ __forceinline__ void vn_sum(const float* __restrict__ c2v, float* __restrict__ P,
-                                       const float* __restrict__ L, const int4* __restrict__ rec, int vs4, int4 t) {
+                                       const float* __restrict__ L, const int4* __restrict__ rec, int vs4, int4 t,
+                                       int zero) {
   const int v = t.x;
   FVec<FV> acc = lds<FV>(L + v * FPC);
   auto add = [&](int slot) {
+    if (VS <= 0 && slot == zero) return;
     const FVec<FV> c = lds<FV>(c2v + slot * FPC);
     if constexpr (FV == 2) {
       const f32x2 t = add2(pack2(acc.v[0], acc.v[1]), pack2(c.v[0], c.v[1]));
@@ -212,6 +217,7 @@ __device__ __forceinline__ void vn_sum(const float* __restrict__ c2v, float* __r
   const int nq = VS > 0 ? VS : vs4;
 #pragma unroll
   for (int q = 1; q < nq; ++q) {
+    if (VS <= 0 && t.w == zero) break;
     t = __ldg(rec + q);
     add(t.x);
     add(t.y);
@@ -225,14 +231,14 @@ __device__ __forceinline__ void vn_sum(const float* __restrict__ c2v, float* __r
 template <int FPC, int FV, int VS>
 __device__ __forceinline__ void vn_sum_range(const float* __restrict__ c2v, float* __restrict__ P,
                                              const float* __restrict__ L, const int4* __restrict__ rec, int vs4,
-                                             int j0, int count, int jstep) {
+                                             int j0, int count, int jstep, int zero) {
   int j = j0;
   for (; j + jstep < count; j += 2 * jstep) {
     const int4 a = __ldg(rec + j * vs4), b = __ldg(rec + (j + jstep) * vs4);
-    vn_sum<FPC, FV, VS>(c2v, P, L, rec + j * vs4, vs4, a);
-    vn_sum<FPC, FV, VS>(c2v, P, L, rec + (j + jstep) * vs4, vs4, b);
+    vn_sum<FPC, FV, VS>(c2v, P, L, rec + j * vs4, vs4, a, zero);
+    vn_sum<FPC, FV, VS>(c2v, P, L, rec + (j + jstep) * vs4, vs4, b, zero);
   }
-  if (j < count) vn_sum<FPC, FV, VS>(c2v, P, L, rec + j * vs4, vs4, __ldg(rec + j * vs4));
+  if (j < count) vn_sum<FPC, FV, VS>(c2v, P, L, rec + j * vs4, vs4, __ldg(rec + j * vs4), zero);
 }
 
 // parity bit of each frame of the vector
@@ -295,14 +301,14 @@ __device__ __forceinline__ void rnd_group(const DevGraph& g, int CS, int vs4, fl
         if (k0 + u < D && r.has(k0 + u)) t[u] = __ldg(all_vn + r.var(k0 + u) * vs4);
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        if (k0 + u < D && r.has(k0 + u)) vn_sum<FPC, FV, VS>(c2v, P, L, all_vn + r.var(k0 + u) * vs4, vs4, t[u]);
+        if (k0 + u < D && r.has(k0 + u)) vn_sum<FPC, FV, VS>(c2v, P, L, all_vn + r.var(k0 + u) * vs4, vs4, t[u], g.n_slots - 1);
     }
   };
   if (live && j0 < cn) {
     if constexpr (D <= 8) {
 #pragma unroll
       for (int k = 0; k < D; ++k)
-        if (cur.has(k)) vn_sum<FPC, FV, VS>(c2v, P, L, all_vn + cur.var(k) * vs4, vs4, t0[k]);
+        if (cur.has(k)) vn_sum<FPC, FV, VS>(c2v, P, L, all_vn + cur.var(k) * vs4, vs4, t0[k], g.n_slots - 1);
     } else {
       resum(cur);
     }
@@ -311,7 +317,13 @@ __device__ __forceinline__ void rnd_group(const DevGraph& g, int CS, int vs4, fl
   __syncthreads();
 }
 
-constexpr int max_threads_for(int D, int FV) { return FV == 2 ? 256 : (D <= 8 ? 512 : (D <= 16 ? 256 : 128)); }
+#ifndef LDPCB_WIDE_THREADS
+#define LDPCB_WIDE_THREADS 256
+#endif
+constexpr int kWideThreads = LDPCB_WIDE_THREADS;  // 16-wide bucket, one frame per thread
+constexpr int max_threads_for(int D, int FV) {
+  return FV == 2 ? 256 : (D <= 8 ? 512 : (D <= 16 ? kWideThreads : 128));
+}
 
 #ifdef LDPCB_PHASE_TIMING
 // Debug build only (scripts/phase_timing.py): CTA-level cycle counts of the
@@ -492,8 +504,8 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
       if (xn > 0) {
         if (live && j0 < xn) {
           const int4* rec = fix_vn + static_cast<size_t>(x0) * vs4;
-          vn_sum<FPC, FV, VS>(c2v, P, L, rec + j0 * vs4, vs4, fix_first);
-          vn_sum_range<FPC, FV, VS>(c2v, P, L, rec, vs4, j0 + jstep, xn, jstep);
+          vn_sum<FPC, FV, VS>(c2v, P, L, rec + j0 * vs4, vs4, fix_first, S - 1);
+          vn_sum_range<FPC, FV, VS>(c2v, P, L, rec, vs4, j0 + jstep, xn, jstep, S - 1);
         }
         __syncthreads();
       }
@@ -512,7 +524,7 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
     // ---- exact totals (decoder.hpp:162-165): removes the rounding of the
     // in-place posterior updates before hard decisions are taken
     if (!RND && g.recompute && (check || !a.lazy_totals)) {
-      if (live) vn_sum_range<FPC, FV, VS>(c2v, P, L, tot_vn, vs4, j0, n, jstep);
+      if (live) vn_sum_range<FPC, FV, VS>(c2v, P, L, tot_vn, vs4, j0, n, jstep, S - 1);
       __syncthreads();
     }
     if (!check) continue;
@@ -567,7 +579,7 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
 finish:
   __syncthreads();
   if (dump) {
-    if (!RND && g.recompute) vn_sum_range<FPC, FV, VS>(c2v, P, L, tot_vn, vs4, j0, n, jstep);
+    if (!RND && g.recompute) vn_sum_range<FPC, FV, VS>(c2v, P, L, tot_vn, vs4, j0, n, jstep, S - 1);
     __syncthreads();
     const int E = g.E;
 #pragma unroll
@@ -786,8 +798,8 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
       if (xn > 0) {
         if (live && j0 < xn) {
           const int4* rec = fix_vn + static_cast<size_t>(x0) * vs4;
-          vn_sum<FPC, FV, VS>(c2v, P, L, rec + j0 * vs4, vs4, fix_first);
-          vn_sum_range<FPC, FV, VS>(c2v, P, L, rec, vs4, j0 + jstep, xn, jstep);
+          vn_sum<FPC, FV, VS>(c2v, P, L, rec + j0 * vs4, vs4, fix_first, S - 1);
+          vn_sum_range<FPC, FV, VS>(c2v, P, L, rec, vs4, j0 + jstep, xn, jstep, S - 1);
         }
         __syncthreads();
       }
@@ -796,7 +808,7 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
     }
     // exact totals, hard decisions, syndrome weights (decoder.hpp:162-171)
     if (!RND && g.recompute) {
-      if (live) vn_sum_range<FPC, FV, VS>(c2v, P, L, tot_vn, vs4, j0, n, jstep);
+      if (live) vn_sum_range<FPC, FV, VS>(c2v, P, L, tot_vn, vs4, j0, n, jstep, S - 1);
       __syncthreads();
     }
     if (live) {
@@ -1246,7 +1258,7 @@ Plan plan_resident(const DevGraph& g, int64_t frames, bool early_stop) {
     if (fv > 0) return fv;
     return (fpc >= 2 && fpc % 2 == 0 && bucket0 <= 8 && !g.per_frame) ? 2 : 1;
   };
-  auto max_threads = [&](int fv) { return fv == 2 ? 256 : (bucket0 <= 8 ? 512 : (bucket0 <= 16 ? 256 : 128)); };
+  auto max_threads = [&](int fv) { return max_threads_for(bucket0 <= 8 ? 8 : (bucket0 <= 16 ? 16 : 32), fv); };
   // one CN item per frame vector for the largest group, in whole warps where
   // that stays a multiple of the frame vectors per CTA
   auto threads_for = [&](int fpc, int fv) {

@@ -486,6 +486,18 @@ KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, boo
     for (int k = 2 + deg; k < t.cs; ++k) out.push_back(-1);
     return mask;
   };
+  // VN records (fix-ups, exact totals) grouped by VN degree, each run in
+  // bank-coloured order: a warp's VNs then have one degree and its record
+  // walk stops at the same padded row (decoder.cu vn_sum). Regular codes: one run.
+  auto order_by_degree = [&](std::vector<int>& vns, uint64_t seed) {
+    auto deg = [&](int v) { return c.var_off[v + 1] - c.var_off[v]; };
+    std::stable_sort(vns.begin(), vns.end(), [&](int a, int b) { return deg(a) < deg(b); });
+    for (int b = 0, e; b < static_cast<int>(vns.size()); b = e) {
+      for (e = b + 1; e < static_cast<int>(vns.size()) && deg(vns[e]) == deg(vns[b]);) ++e;
+      bank_order_vns(vns, b, e, c, t.edge_slot, lay.colour,
+                     b == 0 ? seed : seed + static_cast<uint64_t>(deg(vns[b])) * 0x9e37ull);
+    }
+  };
   t.cn_off.assign(1, 0);
   t.fix_off.assign(1, 0);
   std::vector<int> touches(c.n, 0);
@@ -507,9 +519,7 @@ KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, boo
     for (int r : cns)
       for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e) touches[c.cols[e]] = 0;
     std::sort(shared_vns.begin(), shared_vns.end());
-    if (c.max_vdeg < 16)
-      bank_order_vns(shared_vns, 0, static_cast<int>(shared_vns.size()), c, t.edge_slot, lay.colour,
-                     0x66697875ull + g);
+    if (c.max_vdeg < 16) order_by_degree(shared_vns, 0x66697875ull + g);
     for (int v : shared_vns) put_vn(t.fix_rec, v);
     t.cn_off.push_back(t.cn_off.back() + static_cast<int>(cns.size()));
     t.fix_off.push_back(t.fix_off.back() + static_cast<int>(shared_vns.size()));
@@ -521,7 +531,7 @@ KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, boo
   std::vector<int> all(c.n);
   for (int v = 0; v < c.n; ++v) all[vp[v]] = v;
   for (int v : all) put_vn(t.all_vn_rec, v);
-  if (c.max_vdeg < 16) bank_order_vns(all, 0, c.n, c, t.edge_slot, lay.colour, 0x616c6cull);
+  if (c.max_vdeg < 16) order_by_degree(all, 0x616c6cull);
   for (int v : all) put_vn(t.tot_vn_rec, v);
   for (int r = 0; r < c.m; ++r) put_cn(t.all_rec, r, nullptr);
   return t;

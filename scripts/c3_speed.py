@@ -21,4 +21,10 @@ for name, s in P.configs.c3_schedules(g).items():
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 3
-        print(f"C3 {name} it={iters} es={es}: {F / ms * 1e3:.4e} frames/s  {P.plan(g, s, F)}", flush=True)
+        fps = F / ms * 1e3
+        line = f"C3 {name} it={iters} es={es}: {fps:.4e} frames/s  {P.plan(g, s, F)}"
+        if not es:  # fixed iterations: CN-edge updates/s and the MUFU fraction (3 MUFU per edge update)
+            eu = fps * iters * s.edge_updates_per_iter
+            peak = torch.cuda.get_device_properties(0).multi_processor_count * 16 * 1965e6
+            line += f"  {eu:.3e} edge updates/s, {3 * eu / peak:.3f} of MUFU peak"
+        print(line, flush=True)
