@@ -241,6 +241,50 @@ __device__ __forceinline__ void vn_sum_range(const float* __restrict__ c2v, floa
   if (j < count) vn_sum<FPC, FV, VS>(c2v, P, L, rec + j * vs4, vs4, __ldg(rec + j * vs4), zero);
 }
 
+// The same re-sum from a 16-bit record (host.hpp KernelTables::fix_rec16):
+// eight fields per 16-byte row, so one row serves a VN of degree <= 7.
+template <int FPC, int FV>
+__device__ __forceinline__ void vn_sum16(const float* __restrict__ c2v, float* __restrict__ P,
+                                         const float* __restrict__ L, const int4* __restrict__ rec, int vs16, int4 t,
+                                         int zero) {
+  const int v = t.x & 0xffff;
+  FVec<FV> acc = lds<FV>(L + v * FPC);
+  auto add = [&](int slot) {
+    if (slot == zero) return;
+    const FVec<FV> c = lds<FV>(c2v + slot * FPC);
+#pragma unroll
+    for (int i = 0; i < FV; ++i) acc.v[i] += c.v[i];
+  };
+  auto add2w = [&](int w) {
+    add(w & 0xffff);
+    add(static_cast<int>(static_cast<unsigned>(w) >> 16));
+  };
+  add(static_cast<int>(static_cast<unsigned>(t.x) >> 16));
+  add2w(t.y);
+  add2w(t.z);
+  add2w(t.w);
+  for (int q = 1; q < vs16 && static_cast<int>(static_cast<unsigned>(t.w) >> 16) != zero; ++q) {
+    t = __ldg(rec + q);
+    add2w(t.x);
+    add2w(t.y);
+    add2w(t.z);
+    add2w(t.w);
+  }
+  sts<FV>(P + v * FPC, acc);
+}
+template <int FPC, int FV>
+__device__ __forceinline__ void vn_sum16_range(const float* __restrict__ c2v, float* __restrict__ P,
+                                               const float* __restrict__ L, const int4* __restrict__ rec, int vs16,
+                                               int j0, int count, int jstep, int zero) {
+  int j = j0;
+  for (; j + jstep < count; j += 2 * jstep) {
+    const int4 a = __ldg(rec + j * vs16), b = __ldg(rec + (j + jstep) * vs16);
+    vn_sum16<FPC, FV>(c2v, P, L, rec + j * vs16, vs16, a, zero);
+    vn_sum16<FPC, FV>(c2v, P, L, rec + (j + jstep) * vs16, vs16, b, zero);
+  }
+  if (j < count) vn_sum16<FPC, FV>(c2v, P, L, rec + j * vs16, vs16, __ldg(rec + j * vs16), zero);
+}
+
 // parity bit of each frame of the vector
 template <int D, bool EXACT, int FPC, int FV>
 __device__ __forceinline__ unsigned parity(const float* __restrict__ P, const int32_t* __restrict__ rec, int cs) {
@@ -366,6 +410,8 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
   const int slots = a.list_slots;
   const int4* const tot_vn = reinterpret_cast<const int4*>(g.tot_vn_rec);  // bank-coloured order
   const int4* const fix_vn = reinterpret_cast<const int4*>(g.fix_rec);
+  const int4* const fix16 = reinterpret_cast<const int4*>(g.fix_rec16);
+  const int vs16 = VS > 0 ? 0 : g.vs16;  // 16-bit fix-up records (multi-row VN records only)
 
   const int64_t f0 = static_cast<int64_t>(blockIdx.x) * FPC;
   const int nf = static_cast<int>(min(static_cast<int64_t>(FPC), a.frames - f0));
@@ -478,7 +524,9 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
       const int x0 = go.z, xn = go.w - go.z;
       const int4 ngo = s_go[grp + 1 < g.G ? grp + 1 : 0];  // one broadcast read, one group ahead
       int4 fix_first = make_int4(0, 0, 0, 0);
-      if (j0 < xn) fix_first = __ldg(fix_vn + static_cast<size_t>(x0 + j0) * vs4);
+      if (j0 < xn)
+        fix_first = vs16 ? __ldg(fix16 + static_cast<size_t>(x0 + j0) * vs16)
+                         : __ldg(fix_vn + static_cast<size_t>(x0 + j0) * vs4);
       // this thread's first record was loaded one group ago; the next group's
       // is requested now, a whole CN + fix-up phase before it is needed (the
       // records come from L2: shared memory leaves little L1)
@@ -503,9 +551,15 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
       // frame re-sums to the value it already holds)
       if (xn > 0) {
         if (live && j0 < xn) {
-          const int4* rec = fix_vn + static_cast<size_t>(x0) * vs4;
-          vn_sum<FPC, FV, VS>(c2v, P, L, rec + j0 * vs4, vs4, fix_first, S - 1);
-          vn_sum_range<FPC, FV, VS>(c2v, P, L, rec, vs4, j0 + jstep, xn, jstep, S - 1);
+          if (vs16) {
+            const int4* rec = fix16 + static_cast<size_t>(x0) * vs16;
+            vn_sum16<FPC, FV>(c2v, P, L, rec + j0 * vs16, vs16, fix_first, S - 1);
+            vn_sum16_range<FPC, FV>(c2v, P, L, rec, vs16, j0 + jstep, xn, jstep, S - 1);
+          } else {
+            const int4* rec = fix_vn + static_cast<size_t>(x0) * vs4;
+            vn_sum<FPC, FV, VS>(c2v, P, L, rec + j0 * vs4, vs4, fix_first, S - 1);
+            vn_sum_range<FPC, FV, VS>(c2v, P, L, rec, vs4, j0 + jstep, xn, jstep, S - 1);
+          }
         }
         __syncthreads();
       }
@@ -691,6 +745,8 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
   const int slots = a.list_slots;
   const int4* const tot_vn = reinterpret_cast<const int4*>(g.tot_vn_rec);
   const int4* const fix_vn = reinterpret_cast<const int4*>(g.fix_rec);
+  const int4* const fix16 = reinterpret_cast<const int4*>(g.fix_rec16);
+  const int vs16 = VS > 0 ? 0 : g.vs16;  // 16-bit fix-up records (multi-row VN records only)
   const int nb = (n + 7) >> 3;
 
   // init_state (decoder.hpp:39-52) of slot ff for frame f (f < 0: idle slot)
@@ -778,7 +834,9 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
       const int x0 = go.z, xn = go.w - go.z;
       const int4 ngo = s_go[grp + 1 < g.G ? grp + 1 : 0];
       int4 fix_first = make_int4(0, 0, 0, 0);
-      if (j0 < xn) fix_first = __ldg(fix_vn + static_cast<size_t>(x0 + j0) * vs4);
+      if (j0 < xn)
+        fix_first = vs16 ? __ldg(fix16 + static_cast<size_t>(x0 + j0) * vs16)
+                         : __ldg(fix_vn + static_cast<size_t>(x0 + j0) * vs4);
       const Rec cur = next_cn;
       if (j0 < ngo.y - ngo.x) next_cn.load(g.cn_rec + static_cast<size_t>(ngo.x + j0) * CS, CS);
       if (live && j0 < cn) {
@@ -797,9 +855,15 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
       pin(fix_first);
       if (xn > 0) {
         if (live && j0 < xn) {
-          const int4* rec = fix_vn + static_cast<size_t>(x0) * vs4;
-          vn_sum<FPC, FV, VS>(c2v, P, L, rec + j0 * vs4, vs4, fix_first, S - 1);
-          vn_sum_range<FPC, FV, VS>(c2v, P, L, rec, vs4, j0 + jstep, xn, jstep, S - 1);
+          if (vs16) {
+            const int4* rec = fix16 + static_cast<size_t>(x0) * vs16;
+            vn_sum16<FPC, FV>(c2v, P, L, rec + j0 * vs16, vs16, fix_first, S - 1);
+            vn_sum16_range<FPC, FV>(c2v, P, L, rec, vs16, j0 + jstep, xn, jstep, S - 1);
+          } else {
+            const int4* rec = fix_vn + static_cast<size_t>(x0) * vs4;
+            vn_sum<FPC, FV, VS>(c2v, P, L, rec + j0 * vs4, vs4, fix_first, S - 1);
+            vn_sum_range<FPC, FV, VS>(c2v, P, L, rec, vs4, j0 + jstep, xn, jstep, S - 1);
+          }
         }
         __syncthreads();
       }

@@ -112,6 +112,11 @@ struct KernelTables {
   bool recompute = false;  // some CN updates a posterior in place
   std::vector<int32_t> cn_off, cn_rec;    // per group
   std::vector<int32_t> fix_off, fix_rec;  // per group: VNs shared by >= 2 CNs
+  // the same fix-up records with 16-bit fields (codes with < 2^16 slots and
+  // VN records longer than one row): [pos, slot_0 .. slot_{d-1}, zero ...] as
+  // uint16, eight per 16-byte row, vs16 rows per record (0: not built)
+  std::vector<int32_t> fix_rec16;
+  int vs16 = 0;
   std::vector<int32_t> all_vn_rec;        // every VN, record p = the VN at position p (decoder.hpp:162-165)
   std::vector<int32_t> tot_vn_rec;        // the same records in bank-coloured order (exact totals)
   std::vector<int32_t> all_rec;           // every CN in index order (syndrome)

@@ -498,6 +498,15 @@ KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, boo
                      b == 0 ? seed : seed + static_cast<uint64_t>(deg(vns[b])) * 0x9e37ull);
     }
   };
+  // 16-bit fix-up records: one 16-byte row holds a VN of degree <= 7
+  if (t.vs4 > 1 && t.n_slots <= 65536 && c.n <= 65536) t.vs16 = (1 + c.max_vdeg + 7) / 8;
+  auto put_vn16 = [&](std::vector<int32_t>& out, int v) {
+    std::vector<uint32_t> f(8 * t.vs16, static_cast<uint32_t>(zero));
+    f[0] = static_cast<uint32_t>(vp[v]);
+    int w = 1;
+    for (int j = c.var_off[v]; j < c.var_off[v + 1]; ++j, ++w) f[w] = static_cast<uint32_t>(t.edge_slot[c.var_edges[j]]);
+    for (size_t i = 0; i < f.size(); i += 2) out.push_back(static_cast<int32_t>(f[i] | (f[i + 1] << 16)));
+  };
   t.cn_off.assign(1, 0);
   t.fix_off.assign(1, 0);
   std::vector<int> touches(c.n, 0);
@@ -521,6 +530,8 @@ KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, boo
     std::sort(shared_vns.begin(), shared_vns.end());
     if (c.max_vdeg < 16) order_by_degree(shared_vns, 0x66697875ull + g);
     for (int v : shared_vns) put_vn(t.fix_rec, v);
+    if (t.vs16)
+      for (int v : shared_vns) put_vn16(t.fix_rec16, v);
     t.cn_off.push_back(t.cn_off.back() + static_cast<int>(cns.size()));
     t.fix_off.push_back(t.fix_off.back() + static_cast<int>(shared_vns.size()));
     t.max_cn_items = std::max(t.max_cn_items, static_cast<int>(cns.size()));

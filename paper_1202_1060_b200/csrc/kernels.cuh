@@ -23,6 +23,8 @@ struct DevGraph {
   const int32_t* cn_rec = nullptr;      // see host.hpp KernelTables
   const int32_t* fix_off = nullptr;     // [G+1]
   const int32_t* fix_rec = nullptr;
+  const int32_t* fix_rec16 = nullptr;   // 16-bit fix-up records (vs16 > 0), resident kernels
+  int vs16 = 0;
   const int32_t* all_vn_rec = nullptr;  // [n] VN records, indexed by VN
   const int32_t* tot_vn_rec = nullptr;  // [n] VN records in bank-coloured order
   const int32_t* all_rec = nullptr;     // [m] CN records, syndrome

@@ -487,3 +487,31 @@ def test_frame_queue_is_bit_identical(P, torch, orc, case):
         os.environ.pop("LDPCB_FRAME_QUEUE", None)
     for k in outs["0"]:
         assert np.array_equal(outs["0"][k], outs["2"][k]), k
+
+
+@pytest.mark.parametrize("case", ["c3_nd", "irregular"])
+def test_fix16_records_are_bit_identical(P, torch, orc, case):
+    """16-bit fix-up records (codes with < 2^16 slots and multi-row VN
+    records) against the 32-bit records: the same adds in the same order,
+    so every output is identical."""
+    if case == "c3_nd":
+        g = P.configs.c3_code()
+        s = P.configs.c3_schedules(g)["ndgsbp"]
+    else:
+        g = P.TannerGraph.irregular(2400, [2, 3, 8], [1200, 960, 240], 6, 5)
+        s = P.GroupSchedule.windows(g, 5, 300, 240)
+    llr = cu(torch, orc.transmit_batch_f32(P.sigma2_from_ebn0(1.75, g.rate), 3, g.n_vars, 0, 1001, THREADS))
+    outs = []
+    try:
+        for off in ("1", None):
+            if off:
+                os.environ["LDPCB_NO_FIX16"] = off
+            else:
+                os.environ.pop("LDPCB_NO_FIX16", None)
+            outs.append(to_np(P.decode_batch(g, s, llr, 15, posterior=True, trace=True)))
+            outs.append(to_np(P.decode_batch(g, s, llr, 10, early_stop=False, posterior=True)))
+    finally:
+        os.environ.pop("LDPCB_NO_FIX16", None)
+    for a, b in ((outs[0], outs[2]), (outs[1], outs[3])):
+        for k in a:
+            assert np.array_equal(a[k], b[k]), k
