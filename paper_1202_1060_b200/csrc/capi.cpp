@@ -105,7 +105,7 @@ struct SchedImpl {
   ldpcb::KernelTables tables;
   std::mutex mu;
   struct Dev {
-    int32_t *cn_off, *cn_rec, *fix_off, *fix_rec, *fix_rec16, *all_vn_rec, *tot_vn_rec, *all_rec, *edge_slot, *vn_pos;
+    int32_t *cn_off, *cn_rec, *fix_off, *fix_rec, *fix_rec16, *tot_rec16, *all_vn_rec, *tot_vn_rec, *all_rec, *edge_slot, *vn_pos;
     std::vector<void*> ptrs;
   };
   std::map<int, Dev> dev;
@@ -125,12 +125,13 @@ struct SchedImpl {
     x.fix_off = upload(tables.fix_off);
     x.fix_rec = upload(tables.fix_rec);
     x.fix_rec16 = upload(tables.fix_rec16);
+    x.tot_rec16 = upload(tables.tot_rec16);
     x.all_vn_rec = upload(tables.all_vn_rec);
     x.tot_vn_rec = upload(tables.tot_vn_rec);
     x.all_rec = upload(tables.all_rec);
     x.edge_slot = upload(tables.edge_slot);
     x.vn_pos = upload(tables.vn_pos);
-    x.ptrs = {x.cn_off,     x.cn_rec,     x.fix_off, x.fix_rec,   x.fix_rec16,
+    x.ptrs = {x.cn_off,     x.cn_rec,     x.fix_off, x.fix_rec,   x.fix_rec16, x.tot_rec16,
               x.all_vn_rec, x.tot_vn_rec, x.all_rec, x.edge_slot, x.vn_pos};
     return dev.emplace(d, std::move(x)).first->second;
   }
@@ -257,6 +258,7 @@ ldpcb::DevGraph dev_graph(ldpcb_code code, ldpcb_schedule s) {
   g.fix_rec = d.fix_rec;
   g.fix_rec16 = t.vs16 && !std::getenv("LDPCB_NO_FIX16") ? d.fix_rec16 : nullptr;
   g.vs16 = g.fix_rec16 ? t.vs16 : 0;
+  g.tot_rec16 = g.vs16 ? d.tot_rec16 : nullptr;
   g.all_vn_rec = d.all_vn_rec;
   g.tot_vn_rec = d.tot_vn_rec;
   g.all_rec = d.all_rec;

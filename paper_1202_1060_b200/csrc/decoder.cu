@@ -412,6 +412,7 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
   const int4* const fix_vn = reinterpret_cast<const int4*>(g.fix_rec);
   const int4* const fix16 = reinterpret_cast<const int4*>(g.fix_rec16);
   const int vs16 = VS > 0 ? 0 : g.vs16;  // 16-bit fix-up records (multi-row VN records only)
+  const int4* const tot16 = reinterpret_cast<const int4*>(g.tot_rec16);
 
   const int64_t f0 = static_cast<int64_t>(blockIdx.x) * FPC;
   const int nf = static_cast<int>(min(static_cast<int64_t>(FPC), a.frames - f0));
@@ -578,7 +579,12 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
     // ---- exact totals (decoder.hpp:162-165): removes the rounding of the
     // in-place posterior updates before hard decisions are taken
     if (!RND && g.recompute && (check || !a.lazy_totals)) {
-      if (live) vn_sum_range<FPC, FV, VS>(c2v, P, L, tot_vn, vs4, j0, n, jstep, S - 1);
+      if (live) {
+        if (vs16)
+          vn_sum16_range<FPC, FV>(c2v, P, L, tot16, vs16, j0, n, jstep, S - 1);
+        else
+          vn_sum_range<FPC, FV, VS>(c2v, P, L, tot_vn, vs4, j0, n, jstep, S - 1);
+      }
       __syncthreads();
     }
     if (!check) continue;
@@ -747,6 +753,7 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
   const int4* const fix_vn = reinterpret_cast<const int4*>(g.fix_rec);
   const int4* const fix16 = reinterpret_cast<const int4*>(g.fix_rec16);
   const int vs16 = VS > 0 ? 0 : g.vs16;  // 16-bit fix-up records (multi-row VN records only)
+  const int4* const tot16 = reinterpret_cast<const int4*>(g.tot_rec16);
   const int nb = (n + 7) >> 3;
 
   // init_state (decoder.hpp:39-52) of slot ff for frame f (f < 0: idle slot)
@@ -872,7 +879,12 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
     }
     // exact totals, hard decisions, syndrome weights (decoder.hpp:162-171)
     if (!RND && g.recompute) {
-      if (live) vn_sum_range<FPC, FV, VS>(c2v, P, L, tot_vn, vs4, j0, n, jstep, S - 1);
+      if (live) {
+        if (vs16)
+          vn_sum16_range<FPC, FV>(c2v, P, L, tot16, vs16, j0, n, jstep, S - 1);
+        else
+          vn_sum_range<FPC, FV, VS>(c2v, P, L, tot_vn, vs4, j0, n, jstep, S - 1);
+      }
       __syncthreads();
     }
     if (live) {

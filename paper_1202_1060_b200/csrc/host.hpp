@@ -116,6 +116,7 @@ struct KernelTables {
   // VN records longer than one row): [pos, slot_0 .. slot_{d-1}, zero ...] as
   // uint16, eight per 16-byte row, vs16 rows per record (0: not built)
   std::vector<int32_t> fix_rec16;
+  std::vector<int32_t> tot_rec16;  // tot_vn_rec with 16-bit fields (vs16 > 0)
   int vs16 = 0;
   std::vector<int32_t> all_vn_rec;        // every VN, record p = the VN at position p (decoder.hpp:162-165)
   std::vector<int32_t> tot_vn_rec;        // the same records in bank-coloured order (exact totals)

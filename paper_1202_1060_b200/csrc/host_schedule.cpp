@@ -544,6 +544,8 @@ KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, boo
   for (int v : all) put_vn(t.all_vn_rec, v);
   if (c.max_vdeg < 16) order_by_degree(all, 0x616c6cull);
   for (int v : all) put_vn(t.tot_vn_rec, v);
+  if (t.vs16)
+    for (int v : all) put_vn16(t.tot_rec16, v);
   for (int r = 0; r < c.m; ++r) put_cn(t.all_rec, r, nullptr);
   return t;
 }

@@ -24,6 +24,7 @@ struct DevGraph {
   const int32_t* fix_off = nullptr;     // [G+1]
   const int32_t* fix_rec = nullptr;
   const int32_t* fix_rec16 = nullptr;   // 16-bit fix-up records (vs16 > 0), resident kernels
+  const int32_t* tot_rec16 = nullptr;   // 16-bit totals records (vs16 > 0), resident kernels
   int vs16 = 0;
   const int32_t* all_vn_rec = nullptr;  // [n] VN records, indexed by VN
   const int32_t* tot_vn_rec = nullptr;  // [n] VN records in bank-coloured order
