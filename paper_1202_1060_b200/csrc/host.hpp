@@ -97,7 +97,8 @@ struct ScheduleData {
 // frame-broadcast load per CN or VN item). c2v lives in "slots": for
 // check-regular codes slot(m, k) = m * slot_stride + k with an ODD stride, so
 // the consecutive CNs of a window hit distinct shared-memory banks; otherwise
-// slot = CN-major edge id. The last slot is always zero (pads VN records).
+// CN r owns (deg r | 1) consecutive slots (odd again, so consecutive CNs of one
+// degree hit distinct banks). The last slot is always zero (pads VN records).
 //   CN record  [slot of edge 0, single-touch mask, pos(v_0) .. pos(v_{d-1}), -1 ...]  cs ints
 //   VN record  [pos(v), slot_0 .. slot_{d-1} (ascending CN), zero slot ...] 4*vs4 ints
 // Bit k of the mask is set when v_k has no other CN in the group: the CN
@@ -107,7 +108,7 @@ struct ScheduleData {
 // the same pre-group messages and write the same values).
 struct KernelTables {
   int cs = 0, vs4 = 0;
-  int slot_stride = 0;     // 0: slot = edge id
+  int slot_stride = 0;     // 0: irregular rows, odd per-CN slot counts
   int n_slots = 0;         // including the zero slot
   bool recompute = false;  // some CN updates a posterior in place
   std::vector<int32_t> cn_off, cn_rec;    // per group

@@ -413,7 +413,13 @@ KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, boo
   t.cs = cs;
   t.vs4 = (1 + c.max_vdeg + 3) / 4;
   t.slot_stride = regular_rows ? (c.max_cdeg | 1) : 0;
-  const long long slots = (t.slot_stride ? static_cast<long long>(c.m) * t.slot_stride : c.E) + 1;
+  // irregular rows: CN r's slots start at slot_base[r], each CN holding an
+  // odd number of slots (deg | 1), so consecutive CNs of one degree in a
+  // warp hit distinct shared-memory banks (an even degree d would repeat
+  // every 32 / gcd(2d, 32) CNs: 8-way conflicts for d = 8)
+  std::vector<long long> slot_base(c.m + 1, 0);
+  for (int r = 0; r < c.m; ++r) slot_base[r + 1] = slot_base[r] + ((c.row_off[r + 1] - c.row_off[r]) | 1);
+  const long long slots = (t.slot_stride ? static_cast<long long>(c.m) * t.slot_stride : slot_base[c.m]) + 1;
   if (slots >= (1ll << 30)) throw std::invalid_argument("code too large for 32-bit edge records");
   t.n_slots = static_cast<int>(slots);
   const int zero = t.n_slots - 1;
@@ -458,7 +464,7 @@ KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, boo
   t.edge_slot.resize(c.E);
   for (int r = 0; r < c.m; ++r)
     for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e)
-      t.edge_slot[e] = t.slot_stride ? r * t.slot_stride + pos[e] : c.row_off[r] + pos[e];
+      t.edge_slot[e] = static_cast<int>(t.slot_stride ? r * t.slot_stride + pos[e] : slot_base[r] + pos[e]);
   auto put_vn = [&](std::vector<int32_t>& out, int v) {
     out.push_back(vp[v]);
     int w = 1;
@@ -472,7 +478,7 @@ KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, boo
     if (one)
       for (int p = 0; p < deg; ++p)
         if ((*one)[c.cols[off + perm[off + p]]]) mask |= 1u << p;
-    const int slot = t.slot_stride ? r * t.slot_stride : off;
+    const int slot = static_cast<int>(t.slot_stride ? r * t.slot_stride : slot_base[r]);
     if (packed) {  // {slot | mask << 24, v0 | v1 << 16, v2 | v3 << 16, v4 | v5 << 16}
       uint32_t w[4] = {static_cast<uint32_t>(slot) | (mask << 24), 0, 0, 0};
       for (int p = 0; p < deg; ++p)
