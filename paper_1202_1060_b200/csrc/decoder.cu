@@ -125,13 +125,34 @@ __device__ __forceinline__ void cn_update(float* __restrict__ c2v, float* __rest
         if (mask & (1u << k)) P[cr.var(k) * FPC] = x[k] + c;
       });
     };
+    // a row of exactly W edges: no padding positions, no per-position predicates
+    auto row_exact = [&](auto width) {
+      constexpr int W = decltype(width)::value;
+      float x[W];
+#pragma unroll
+      for (int k = 0; k < W; ++k) x[k] = P[cr.var(k) * FPC] - c2v[(base + k) * FPC];
+      boxplus_row<W, true>(x, W, [&](int k, float c) {
+        c2v[(base + k) * FPC] = c;
+        if (mask & (1u << k)) P[cr.var(k) * FPC] = x[k] + c;
+      });
+    };
     // wide buckets: rows of degree <= 8 (most QC block rows; warps are
-    // homogeneous because a group lists whole block rows) take the 8-wide
-    // code, whose predicated-off positions no longer cost issue slots
+    // homogeneous because a group lists whole block rows) take code of their
+    // exact width (padding with the boxplus identity (0, 1) is exact, so the
+    // outputs are those of the 8-wide code), degree-3..8 rows without padding
     if constexpr (!EXACT && D > 8) {
-      if (deg <= 8) {
-        row(std::integral_constant<int, 8>{});
-        return;
+      switch (deg) {
+        case 3: row_exact(std::integral_constant<int, 3>{}); return;
+        case 4: row_exact(std::integral_constant<int, 4>{}); return;
+        case 5: row_exact(std::integral_constant<int, 5>{}); return;
+        case 6: row_exact(std::integral_constant<int, 6>{}); return;
+        case 7: row_exact(std::integral_constant<int, 7>{}); return;
+        case 8: row_exact(std::integral_constant<int, 8>{}); return;
+        default:
+          if (deg <= 8) {
+            row(std::integral_constant<int, 8>{});
+            return;
+          }
       }
     }
     row(std::integral_constant<int, D>{});
