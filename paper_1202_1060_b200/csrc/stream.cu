@@ -46,9 +46,11 @@ struct ChunkState {
 // kernel to complete (and its writes to be visible) before touching state.
 // The next kernel's CTAs are placed as this kernel's last wave drains, which
 // hides the launch gap between ~900 dependent launches per chunk.
+__device__ __forceinline__ void pdl_launch_next() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_enter() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  pdl_launch_next();
+  pdl_wait();
 }
 
 // V consecutive frames per thread: one V*4-byte vector access per element
@@ -127,15 +129,18 @@ __global__ void stream_init(int n, const int32_t* __restrict__ pos, const float*
 // CN phase of one group over (record, V-frame vector) items.
 template <int D, bool EXACT, int V>
 __global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ recs, int CS, int count, ChunkState s) {
-  pdl_enter();
+  pdl_launch_next();
   const int64_t QB = s.B / V;
   const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (item >= count * QB) return;
   const int j = static_cast<int>(item / QB);
   const int64_t q = item - j * QB;
+  // the CN record is a constant table: requested before waiting for the
+  // previous kernel, so its latency overlaps that kernel's drain
+  const CnRecord<D, EXACT> cr(recs + static_cast<int64_t>(j) * CS, CS);
+  pdl_wait();
   const unsigned dn = done_bits<V>(s, q);
   if (dn == (1u << V) - 1) return;
-  const CnRecord<D, EXACT> cr(recs + static_cast<int64_t>(j) * CS, CS);
   const int base = cr.slot();
   const unsigned mask = cr.mask();
   const int deg = cr.deg();
@@ -184,15 +189,16 @@ __global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ rec
 template <int V>
 __global__ void __launch_bounds__(256) stream_vnsum(const int4* __restrict__ recs, int vs4, int count, ChunkState s,
                                                     int skip_done) {
-  pdl_enter();
+  pdl_launch_next();
   const int64_t QB = s.B / V;
   const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (item >= count * QB) return;
   const int j = static_cast<int>(item / QB);
   const int64_t q = item - j * QB;
-  if (skip_done && done_bits<V>(s, q) == (1u << V) - 1) return;
   const int4* rec = recs + static_cast<int64_t>(j) * vs4;
-  int4 t = __ldg(rec);
+  int4 t = __ldg(rec);  // constant table: requested before the wait
+  pdl_wait();
+  if (skip_done && done_bits<V>(s, q) == (1u << V) - 1) return;
   const int v = t.x;
   Vec<V> acc = ldv<V>(s.L + static_cast<int64_t>(v) * s.B + V * q);
   auto add = [&](int slot) {
