@@ -1,20 +1,27 @@
 #!/usr/bin/env python
 """Throughput benchmark: BASELINE.json's metric (decoded info bits/s at fixed
-iterations) on its throughput configuration (config 5).
+iterations) on its throughput configuration (config 5), both codes.
 
-Default workload "c5_n1008": the (3,6)-regular n=1008 code with 4-cycles
-removed, NDGSBP (8 windows of 84 CNs at stride 63), Eb/N0 = 2.0 dB, exactly 10
-iterations (no early stop). One step = one decode of a batch of frames per GPU
-whose fp32 LLRs are already resident in HBM (generated on the device with the
-reference's channel stream, frame ids sharded by rank), followed by the NCCL
-allreduce of the int64[6] error / iteration counters.
+Config 5 names two workloads, and the default run measures both:
+  c5_n1008   the (3,6)-regular n=1008 code with 4-cycles removed, NDGSBP
+             (8 windows of 84 CNs at stride 63), Eb/N0 = 2.0 dB: decoded by
+             the shared-memory-resident kernel. The headline (top-level keys).
+  c5_n64800  the irregular n=64800 code, NDGSBP (45 windows of 960 at stride
+             720), Eb/N0 = 1.1 dB: decoded by the HBM-streamed kernels.
+             Reported under "legs" with the same keys.
+Both: exactly 10 iterations (no early stop). One step = one decode of a batch
+of frames per GPU whose fp32 LLRs are already resident in HBM (generated on
+the device with the reference's channel stream, frame ids sharded by rank),
+followed by the NCCL allreduce of the int64[6] error / iteration counters.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference]
+                  [--workload c5|c5_n1008|c5_n64800]
 
 Under torchrun each rank decodes its own frame range (weak scaling); rank 0
 prints one JSON line. `--impl reference` runs the reference CPU decoder
 (oracle/_ref: the unmodified reference headers, else the C port) on all host
-cores on a bounded sample of the same workload.
+cores on a bounded sample of the same workloads; that process reads the
+codes from bench_fixtures/c5_workloads.npz and never loads the product.
 """
 from __future__ import annotations
 
@@ -27,6 +34,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -37,6 +46,12 @@ MUFU_PER_SM_CLK = 16
 HBM_BYTES_PER_EDGE = 8  # streamed decoder: c2v read + write per CN-edge update (fp32)
 HBM_BYTES_PER_TOUCH = 8  # posterior read + write per distinct VN a group touches (fp32)
 DEFAULT_FRAMES = {"c5_n1008": 1 << 21, "c5_n64800": 8192}
+FIXTURE = os.path.join(ROOT, "bench_fixtures", "c5_workloads.npz")
+DESC = {
+    "c5_n1008": "C5: (3,6)-regular n=1008 girth>=6 (seed 1), NDGSBP 8 windows x 84 CNs stride 63, Eb/N0 2.0 dB",
+    "c5_n64800": ("C5: irregular n=64800 VN degrees {2:.5,3:.4,8:.1} d_c=6 (seed 1), NDGSBP 45 windows x 960 CNs "
+                  "stride 720, Eb/N0 1.1 dB"),
+}
 
 
 def parse():
@@ -45,10 +60,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", default="c5_n1008")
+    ap.add_argument("--workload", default="c5", choices=["c5", "c5_n1008", "c5_n64800"],
+                    help="c5 = both config-5 codes (n=1008 headline + n=64800 leg)")
     ap.add_argument("--frames", type=int, default=0, help="frames per step per GPU (0: per-workload default)")
     ap.add_argument("--iters", type=int, default=10)
-    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU sample duration")
+    ap.add_argument("--cpu-seconds", type=float, default=30.0, help="CPU sample duration per workload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fpc", type=int, default=0, help="frames per CTA (0 = library plan)")
@@ -56,25 +72,18 @@ def parse():
     return ap.parse_args()
 
 
-def workload(name):
-    import paper_1202_1060_b200 as P
-
-    if name == "c5_n1008":
-        g = P.configs.c1_code()
-        s = P.configs.c1_schedules(g)["ndgsbp"]
-        desc = "C5: (3,6)-regular n=1008 girth>=6 (seed 1), NDGSBP 8 windows x 84 CNs stride 63, Eb/N0 2.0 dB"
-        return g, s, 2.0, desc
-    if name == "c5_n64800":
-        g = P.configs.c4_code()
-        s = P.configs.c4_schedules(g)["ndgsbp"]
-        desc = ("C5: irregular n=64800 VN degrees {2:.5,3:.4,8:.1} d_c=6 (seed 1), NDGSBP 45 windows x 960 CNs "
-                "stride 720, Eb/N0 1.1 dB")
-        return g, s, 1.1, desc
-    raise SystemExit(f"unknown workload {name}")
+def leg_names(args):
+    return ["c5_n1008", "c5_n64800"] if args.workload == "c5" else [args.workload]
 
 
-def mean_sigma2(P, g, ebn0):
-    return P.sigma2_from_ebn0(ebn0, g.rate)
+def fixture(name):
+    """(n, row_off, cols, groups, ebn0, edge_updates_per_iter) of a config-5
+    workload from the committed fixture (scripts/make_bench_fixture.py)."""
+    z = np.load(FIXTURE)
+    off, cns = z[f"{name}_grp_off"], z[f"{name}_grp_cns"]
+    groups = [cns[off[i]:off[i + 1]].tolist() for i in range(len(off) - 1)]
+    return (int(z[f"{name}_n"]), z[f"{name}_row_off"], z[f"{name}_cols"], groups, float(z[f"{name}_ebn0"]),
+            int(z[f"{name}_edge_updates_per_iter"]))
 
 
 class ClockSampler:
@@ -134,89 +143,119 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def reference_cpu(g, s, sigma2, iters, target_s, frames_hint=None):
-    """Time the reference CPU decoder on all host threads on a bounded sample.
-    Returns (info_bits_per_s, frames, seconds, threads, kind)."""
-    from oracle.oracle import best_available
+class CpuReference:
+    """The reference decoder on all host threads (oracle/_ref when built, else
+    the C port), fixed iterations, one bounded sample per call. Frame ids
+    pull from an atomic counter inside the oracle (sim.hpp:136-150)."""
 
-    orc = best_available()
-    threads = os.cpu_count() or 1
-    og = orc.graph(g.n_vars, *g.csr())
-    groups = s.groups
-    K = g.n_vars - g.n_checks
-    cal = max(threads * 4, 64)
-    llr = orc.transmit_batch_f32(sigma2, 1, g.n_vars, 0, cal, threads)
-    t0 = time.perf_counter()
-    orc.decode_batch(og, groups, llr, iters, early_stop=False, threads=threads)
-    dt = time.perf_counter() - t0
-    frames = frames_hint or max(cal, int(cal * target_s / max(dt, 1e-6)))
-    llr = orc.transmit_batch_f32(sigma2, 1, g.n_vars, 0, frames, threads)
-    t0 = time.perf_counter()
-    orc.decode_batch(og, groups, llr, iters, early_stop=False, threads=threads)
-    dt = time.perf_counter() - t0
-    return frames * K / dt, frames, dt, threads, orc.kind
+    def __init__(self, name, iters):
+        from oracle.oracle import best_available
+
+        self.orc = best_available()
+        n, row_off, cols, self.groups, ebn0, _ = fixture(name)
+        self.n, self.m = n, len(row_off) - 1
+        self.K = n - self.m
+        self.iters = iters
+        self.g = self.orc.graph(n, row_off, cols)
+        self.sigma2 = self.orc.sigma2_from_ebn0(ebn0, self.K / n)
+        self.threads = os.cpu_count() or 1
+        self._llr = None
+
+    def llr(self, frames):
+        if self._llr is None or len(self._llr) < frames:
+            self._llr = self.orc.transmit_batch_f32(self.sigma2, 1, self.n, 0, frames, self.threads)
+        return self._llr[:frames]
+
+    def run(self, frames):
+        """Decodes `frames` frames; returns the wall time."""
+        x = self.llr(frames)
+        t0 = time.perf_counter()
+        self.orc.decode_batch(self.g, self.groups, x, self.iters, early_stop=False, threads=self.threads)
+        return time.perf_counter() - t0
+
+    def frames_for(self, seconds):
+        """Frames that take about `seconds` (one calibration decode)."""
+        cal = max(2 * self.threads, 16)
+        dt = self.run(cal)
+        return max(self.threads, int(cal * seconds / max(dt, 1e-6)))
+
+    def baseline(self, seconds):
+        """One timed sample of about `seconds` -> cpu_baseline dict."""
+        frames = self.frames_for(seconds)
+        dt = self.run(frames)
+        return {"value": frames * self.K / dt, "unit": UNIT, "cores": self.threads, "kind": self.orc.kind,
+                "sample": f"{frames} frames of the same workload, {self.iters} fixed iterations ({dt:.1f} s, "
+                          f"{self.threads} threads)"}
+
+
+def reference_leg(args, name):
+    ref = CpuReference(name, args.iters)
+    per_step = max(args.cpu_seconds / max(args.steps, 1), 1.0)
+    frames = ref.frames_for(per_step)
+    warm = max(ref.threads, frames // 4)
+    for _ in range(args.warmup):
+        ref.run(warm)
+    times = [ref.run(frames) for _ in range(args.steps)]
+    value = frames * ref.K / statistics.median(times)
+    return {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "ms_per_step": statistics.median(times) * 1e3,
+        "config": {"workload": DESC[name] + f", {args.iters} fixed iterations", "frames_per_step": frames,
+                   "host_threads": ref.threads},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": ref.threads, "kind": ref.orc.kind,
+                         "sample": f"{frames} frames per step x {args.steps} steps ({sum(times):.1f} s timed), "
+                                   f"{args.warmup} warm-up steps of {warm} frames"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import paper_1202_1060_b200 as P
-
-    g, s, ebn0, desc = workload(args.workload)
-    sigma2 = mean_sigma2(P, g, ebn0)
-    per_step = max(1.0, args.cpu_seconds / max(args.steps, 1))
-    vals = []
-    info = None
-    for i in range(args.warmup + args.steps):
-        v, frames, dt, threads, kind = reference_cpu(g, s, sigma2, args.iters, per_step,
-                                                     frames_hint=info[1] if info else None)
-        info = (v, frames, dt, threads, kind)
-        if i >= args.warmup:
-            vals.append((v, dt))
-    value = statistics.median(v for v, _ in vals)
-    ms = statistics.median(dt for _, dt in vals) * 1e3
+    names = leg_names(args)
+    legs = {nm: reference_leg(args, nm) for nm in names}
+    head = legs[names[0]]
     line = {
         "impl": "reference",
-        "metric": METRIC,
-        "value": value,
-        "unit": UNIT,
+        **{k: head[k] for k in ("metric", "value", "unit")},
         "n_gpus": args.gpus,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": ms,
+        "ms_per_step": head["ms_per_step"],
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (reference channel stream, seed 1)",
-        "config": {"workload": desc + f", {args.iters} fixed iterations", "frames_per_step": info[1],
-                   "host_threads": info[3]},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": info[3], "kind": info[4],
-                         "sample": f"{info[1]} frames per step of the same workload"},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": head["config"],
+        "cpu_baseline": head["cpu_baseline"],
+        "e2e": head["e2e"],
+        "legs": {nm: legs[nm] for nm in names[1:]},
     }
     print(json.dumps(line), flush=True)
 
 
-def run_b200(args):
+def measure_leg(args, name, world, rank, local):
     import torch
     import torch.distributed as dist
 
     import paper_1202_1060_b200 as P
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-
-    g, s, ebn0, desc = workload(args.workload)
-    sigma2 = mean_sigma2(P, g, ebn0)
+    if name == "c5_n1008":
+        g = P.configs.c1_code()
+        s = P.configs.c1_schedules(g)["ndgsbp"]
+        ebn0 = 2.0
+    else:
+        g = P.configs.c4_code()
+        s = P.configs.c4_schedules(g)["ndgsbp"]
+        ebn0 = 1.1
+    sigma2 = P.sigma2_from_ebn0(ebn0, g.rate)
     P.set_tuning(args.fpc, args.threads)
-    B = args.frames or DEFAULT_FRAMES[args.workload]
+    B = args.frames or DEFAULT_FRAMES[name]
     n = g.n_vars
     K = n - g.n_checks
     stream = torch.cuda.current_stream()
@@ -284,7 +323,7 @@ def run_b200(args):
     tf = os.path.join(ROOT, "profiles", "dram_bytes_per_frame.json")
     if os.path.exists(tf):
         try:
-            rec = json.load(open(tf)).get(args.workload)
+            rec = json.load(open(tf)).get(name)
             if rec:
                 traffic = rec["bytes_per_frame"] * B / 1e9
         except (OSError, ValueError, KeyError):
@@ -313,8 +352,7 @@ def run_b200(args):
                             f"{s.edge_updates_per_iter} CN-edge updates + {HBM_BYTES_PER_TOUCH} B x "
                             f"{s.touched_per_iter} touched VNs) + LLR in + bits out, x {B} frames / CUDA-event time "
                             f"{kernel_ms:.3f} ms; peak = MEASURED_PEAKS hbm_gbs; traffic = ncu DRAM bytes of all "
-                            "stream kernels per frame (profiles/dram_bytes_per_frame.json, one 8192-frame decode) "
-                            "x frames: 1.05x the algorithmic bytes (syndrome, init and bit-packing passes)"}
+                            "stream kernels per frame (profiles/dram_bytes_per_frame.json) x frames"}
 
     # ---- end to end through the host C-ABI call (pinned host buffers)
     e2e = None
@@ -349,52 +387,79 @@ def run_b200(args):
         c1.record(stream)
         torch.cuda.synchronize()
         link_gbs = 3 * Be * n * 4 / (c0.elapsed_time(c1) / 1e3) / 1e9
-        del d_tmp
+        del d_tmp, h_llr, h_bits
         e2e = {"value": Be * e_steps * world * K / e_dt, "unit": UNIT, "h2d_bytes_per_step": Be * n * 4,
                "d2h_bytes_per_step": Be * ((n + 7) // 8) + 48,
                "api": "ldpcb_decode_host (pinned host LLRs in, packed bits + counters out)",
                "h2d_gbs": round(Be * n * 4 * e_steps / e_dt / 1e9, 2),
                "h2d_link_gbs": round(link_gbs, 2),
                "note": "h2d_gbs = LLR bytes / e2e step time; h2d_link_gbs = a bare pinned copy of the same bytes"}
+    del llr
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, frames, dt, threads, kind = reference_cpu(g, s, sigma2, args.iters, args.cpu_seconds)
-        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
-               "sample": f"{frames} frames of the same workload ({dt:.1f} s, {threads} threads)"}
+        cpu = CpuReference(name, args.iters).baseline(args.cpu_seconds)
+
+    return {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "ms_per_step": elapsed_ms / args.steps,
+        "config": {
+            "workload": DESC[name] + f", {args.iters} fixed iterations, no early stop",
+            "frames_per_step_per_gpu": B,
+            "parallelism": f"frames sharded over {world} GPU(s), NCCL allreduce of int64[6] counters",
+            "l2": f"inputs ({B * n * 4 / 1e9:.1f} GB per GPU) larger than L2; no flush",
+            "plan": pl,
+        },
+        "frames_per_s": total_frames / (elapsed_ms / 1e3),
+        "edge_updates_per_s": edge_updates * args.steps * world / (elapsed_ms / 1e3),
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "counters": dict(zip(P.COUNTER_NAMES, cnt)),
+    }
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    names = leg_names(args)
+    legs = {}
+    for nm in names:
+        legs[nm] = measure_leg(args, nm, world, rank, local)
+        torch.cuda.empty_cache()
 
     if world > 1:
         dist.barrier()
     if rank == 0:
-        clocks = clk.summary()
+        head = legs[names[0]]
         line = {
             "metric": METRIC,
-            "value": value,
+            "value": head["value"],
             "unit": UNIT,
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
-            "ms_per_step": elapsed_ms / args.steps,
+            "ms_per_step": head["ms_per_step"],
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
             "dtype": "f32",
             "data": "synthetic (device port of the reference channel stream, seed 1)",
-            "config": {
-                "workload": desc + f", {args.iters} fixed iterations, no early stop",
-                "frames_per_step_per_gpu": B,
-                "parallelism": f"frames sharded over {world} GPU(s), NCCL allreduce of int64[6] counters",
-                "l2": f"inputs ({B * n * 4 / 1e9:.1f} GB per GPU) larger than L2; no flush",
-                "plan": pl,
-            },
-            "frames_per_s": total_frames / (elapsed_ms / 1e3),
-            "edge_updates_per_s": edge_updates * args.steps * world / (elapsed_ms / 1e3),
-            "roofline": roofline,
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": launches,
-            "clocks": clocks,
-            "counters": dict(zip(P.COUNTER_NAMES, cnt)),
+            **{k: head[k] for k in ("config", "frames_per_s", "edge_updates_per_s", "roofline", "cpu_baseline",
+                                    "e2e", "gpu_launches", "clocks", "counters")},
+            "legs": {nm: legs[nm] for nm in names[1:]},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

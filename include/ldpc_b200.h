@@ -164,6 +164,24 @@ int ldpcb_simulate_frames_device(ldpcb_code code, ldpcb_schedule s, double sigma
 int ldpcb_run_sweep_host(ldpcb_code code, ldpcb_schedule s, const double *ebn0_db, int n_points, int iter_limit,
                          int64_t max_frames, int min_frame_errors, uint64_t channel_seed, int64_t wave_frames,
                          double *out);
+/* ---- several GPUs of one process --------------------------------------
+ * One host thread per entry of devices[] (the reference's worker pool,
+ * sim.hpp:136-150, with a GPU per worker); frame ids are split into
+ * contiguous ranges in list order, frame i of n_devices getting
+ * [begin + F*i/n, begin + F*(i+1)/n); frames are keyed by id, so results do
+ * not depend on the device count. A device may be listed more than once.
+ * Counters are summed on the host (the single-process counterpart of the
+ * NCCL allreduce used by one-process-per-GPU jobs). Blocks until done. */
+/* simulate over several GPUs: counters (host int64[6]) accumulated */
+int ldpcb_simulate_multi(ldpcb_code code, ldpcb_schedule s, const int *devices, int n_devices, double sigma2,
+                         uint64_t channel_seed, int64_t frame_begin, int64_t frames, int max_iters, int early_stop,
+                         int64_t *counters);
+/* run_sweep (sim.hpp:96-186) over several GPUs: every wave is split over the
+ * devices and the min-frame-errors prefix stop is taken on the gathered
+ * per-frame outcomes in frame order; out as ldpcb_run_sweep_host */
+int ldpcb_run_sweep_multi(ldpcb_code code, ldpcb_schedule s, const int *devices, int n_devices,
+                          const double *ebn0_db, int n_points, int iter_limit, int64_t max_frames,
+                          int min_frame_errors, uint64_t channel_seed, int64_t wave_frames, double *out);
 /* ldpcb_simulate_device with host counters; blocks until done */
 int ldpcb_simulate_host(ldpcb_code code, ldpcb_schedule s, double sigma2, uint64_t channel_seed, int64_t frame_begin,
                         int64_t frames, int max_iters, int early_stop, int64_t *counters);

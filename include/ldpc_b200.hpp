@@ -318,6 +318,19 @@ inline std::array<int64_t, 6> simulate(const TannerGraph& g, const GroupSchedule
   return c;
 }
 
+// simulate over several GPUs (ldpcb_simulate_multi): one host thread per
+// entry of `devices`, contiguous frame-id ranges, counters summed
+inline std::array<int64_t, 6> simulate(const TannerGraph& g, const GroupSchedule& s, double ebn0_db,
+                                       std::uint64_t channel_seed, int64_t frame_begin, int64_t frames,
+                                       int max_iters, bool early_stop, const std::vector<int>& devices) {
+  const double rate = static_cast<double>(g.n_vars - g.n_checks) / g.n_vars;  // sim.hpp:103
+  std::array<int64_t, 6> c{};
+  detail::check(ldpcb_simulate_multi(g.handle(), s.handle(), devices.data(), static_cast<int>(devices.size()),
+                                     sigma2_from_ebn0(ebn0_db, rate), channel_seed, frame_begin, frames, max_iters,
+                                     early_stop ? 1 : 0, c.data()));
+  return c;
+}
+
 // SimResult (sim.hpp:44-56)
 struct SimResult {
   double ebn0_db = 0.0;
@@ -336,12 +349,20 @@ struct SimResult {
 // run_sweep (sim.hpp:96-186) on the calling thread's GPU: frames 0,1,... per
 // point until the smallest prefix holding min_frame_errors frame errors, or
 // max_frames. Pass make_per_frame_schedule for the harness's own grouping.
+// With a non-empty `devices` list every wave is split over those GPUs
+// (ldpcb_run_sweep_multi); the result is the same for any device list.
 inline std::vector<SimResult> run_sweep(const TannerGraph& g, const GroupSchedule& s,
                                         const std::vector<double>& ebn0_db, int iter_limit, long max_frames,
-                                        int min_frame_errors, std::uint64_t channel_seed = 1) {
+                                        int min_frame_errors, std::uint64_t channel_seed = 1,
+                                        const std::vector<int>& devices = {}) {
   std::vector<double> raw(11 * ebn0_db.size());
-  detail::check(ldpcb_run_sweep_host(g.handle(), s.handle(), ebn0_db.data(), static_cast<int>(ebn0_db.size()),
-                                     iter_limit, max_frames, min_frame_errors, channel_seed, 0, raw.data()));
+  if (devices.empty())
+    detail::check(ldpcb_run_sweep_host(g.handle(), s.handle(), ebn0_db.data(), static_cast<int>(ebn0_db.size()),
+                                       iter_limit, max_frames, min_frame_errors, channel_seed, 0, raw.data()));
+  else
+    detail::check(ldpcb_run_sweep_multi(g.handle(), s.handle(), devices.data(), static_cast<int>(devices.size()),
+                                        ebn0_db.data(), static_cast<int>(ebn0_db.size()), iter_limit, max_frames,
+                                        min_frame_errors, channel_seed, 0, raw.data()));
   std::vector<SimResult> out(ebn0_db.size());
   for (std::size_t i = 0; i < out.size(); ++i) {
     const double* o = raw.data() + 11 * i;

@@ -28,8 +28,10 @@ from .api import (  # noqa: F401
     set_lazy_totals,
     set_tuning,
     sigma2_from_ebn0,
+    run_sweep_multi,
     run_sweep_native,
     simulate,
+    simulate_multi,
     simulate_frames,
     transmit_all_zero,
 )

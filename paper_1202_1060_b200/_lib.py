@@ -68,6 +68,8 @@ _SIGS = {
         [vp, vp, i64, vp, C.c_int, C.c_int, vp, C.c_int, vp, vp, vp, vp, vp],
     ),
     "ldpcb_simulate_host": (C.c_int, [vp, vp, dbl, u64, i64, i64, C.c_int, C.c_int, vp]),
+    "ldpcb_simulate_multi": (C.c_int, [vp, vp, vp, C.c_int, dbl, u64, i64, i64, C.c_int, C.c_int, vp]),
+    "ldpcb_run_sweep_multi": (C.c_int, [vp, vp, vp, C.c_int, vp, C.c_int, C.c_int, i64, C.c_int, u64, i64, vp]),
     "ldpcb_simulate_device": (C.c_int, [vp, vp, dbl, u64, i64, i64, C.c_int, C.c_int, vp, vp]),
     "ldpcb_check_update_device": (C.c_int, [C.c_int, i64, vp, vp, vp]),
     "ldpcb_run_subiterations_device": (C.c_int, [vp, vp, i64, vp, C.c_int, vp, vp, vp]),

@@ -362,6 +362,7 @@ def decode_batch(
     optionally posterior, syndrome_trace. `counters` (int64[6] cuda tensor)
     is accumulated into when given."""
     torch = _torch()
+    _device_counters(counters)
     if llr.dtype != torch.float32 or not llr.is_cuda or not llr.is_contiguous():
         raise ValueError("llr must be a contiguous float32 CUDA tensor")
     if llr.dim() != 2 or llr.shape[1] != g.n_vars:
@@ -401,6 +402,43 @@ def decode_batch(
     return out
 
 
+_NP_OF_TORCH = {"torch.float32": np.float32, "torch.uint8": np.uint8, "torch.int32": np.int32,
+                "torch.int64": np.int64}
+
+
+def _host_check(a, dtype, size, name):
+    """Host buffer passed as a raw pointer: C-contiguous, host-resident, the
+    given dtype and (when size is not None) exactly `size` elements. Returns
+    the leading dimension."""
+    if a is None:
+        return 0
+    if isinstance(a, np.ndarray):
+        ok_dtype = a.dtype == np.dtype(dtype)
+        contiguous = a.flags["C_CONTIGUOUS"]
+        count = a.size
+    else:  # torch.Tensor on the host (pinned or pageable)
+        if a.is_cuda:
+            raise ValueError(f"{name} must be a host buffer")
+        ok_dtype = _NP_OF_TORCH.get(str(a.dtype)) is dtype
+        contiguous = a.is_contiguous()
+        count = a.numel()
+    if not ok_dtype:
+        raise ValueError(f"{name} must be {np.dtype(dtype).name}, got {a.dtype}")
+    if not contiguous:
+        raise ValueError(f"{name} must be C-contiguous")
+    if size is not None and count != size:
+        raise ValueError(f"{name} must hold exactly {size} elements, got {count}")
+    return a.shape[0] if a.ndim else 0
+
+
+def _device_counters(counters, name="counters"):
+    if counters is None:
+        return
+    if not getattr(counters, "is_cuda", False) or str(counters.dtype) != "torch.int64" or counters.numel() != 6 \
+            or not counters.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous int64[6] CUDA tensor")
+
+
 def decode_host(
     g: TannerGraph,
     s: GroupSchedule,
@@ -415,8 +453,22 @@ def decode_host(
     counters=None,
     syndrome_trace=None,
 ):
-    """decode() from host memory (numpy / pinned torch CPU tensors); blocks."""
-    F = llr.shape[0]
+    """decode() from host memory (numpy / pinned torch CPU tensors); blocks.
+
+    The library reads LLRs as fp32 and writes every output with a D2H copy of
+    its exact size, so dtypes and sizes are checked here (a float64 array, the
+    reference decoder's own LLR type, is rejected instead of being read as
+    fp32 garbage)."""
+    F = _host_check(llr, np.float32, None, "llr")
+    if llr.ndim != 2 or llr.shape[1] != g.n_vars:
+        raise ValueError("channel LLR length does not match the code length")
+    n = g.n_vars
+    _host_check(bits, np.uint8, F * ((n + 7) // 8 if packed else n), "bits")
+    _host_check(iterations, np.int32, F, "iterations")
+    _host_check(converged, np.uint8, F, "converged")
+    _host_check(posterior, np.float32, F * n, "posterior")
+    _host_check(syndrome_trace, np.int32, F * max_iters, "syndrome_trace")
+    _host_check(counters, np.int64, 6, "counters")
     check(
         lib.ldpcb_decode_host(
             g.handle,
@@ -444,6 +496,7 @@ def simulate(g, s, sigma2: float, channel_seed: int, frame_begin: int, frames: i
     torch = _torch()
     if counters is None:
         counters = torch.zeros(6, dtype=torch.int64, device="cuda")
+    _device_counters(counters)
     check(
         lib.ldpcb_simulate_device(
             g.handle, s.handle, sigma2, channel_seed, frame_begin, frames, max_iters, int(early_stop),
@@ -484,6 +537,37 @@ def run_sweep_native(g, s, ebn0_db, iter_limit: int, max_frames: int, min_frame_
             "mean_iters_all", "iter_limit", "wall_seconds", "ebn0_db")
     ints = {"frames", "bit_errors", "frame_errors", "converged_frames", "iter_limit"}
     return [{k: (int(v) if k in ints else float(v)) for k, v in zip(keys, row)} for row in out]
+
+
+def _sweep_records(out) -> list[dict]:
+    keys = ("frames", "bit_errors", "frame_errors", "converged_frames", "ber", "fer", "mean_iters_converged",
+            "mean_iters_all", "iter_limit", "wall_seconds", "ebn0_db")
+    ints = {"frames", "bit_errors", "frame_errors", "converged_frames", "iter_limit"}
+    return [{k: (int(v) if k in ints else float(v)) for k, v in zip(keys, row)} for row in out]
+
+
+def simulate_multi(g, s, devices, sigma2: float, channel_seed: int, frame_begin: int, frames: int, max_iters: int,
+                   early_stop: bool = True) -> np.ndarray:
+    """ldpcb_simulate_multi: frames [frame_begin, frame_begin+frames) split in
+    contiguous ranges over `devices` (one host thread per entry, a device may
+    repeat); returns the summed int64[6] counters (host)."""
+    dev = np.ascontiguousarray(list(devices), np.int32)
+    cnt = np.zeros(6, np.int64)
+    check(lib.ldpcb_simulate_multi(g.handle, s.handle, _vp(dev), len(dev), sigma2, channel_seed, frame_begin, frames,
+                                   max_iters, int(early_stop), _vp(cnt)), "simulate_multi")
+    return cnt
+
+
+def run_sweep_multi(g, s, devices, ebn0_db, iter_limit: int, max_frames: int, min_frame_errors: int,
+                    channel_seed: int = 1, wave_frames: int = 0) -> list[dict]:
+    """run_sweep (sim.hpp:96-186) over several GPUs through ldpcb_run_sweep_multi."""
+    dev = np.ascontiguousarray(list(devices), np.int32)
+    pts = np.ascontiguousarray(list(ebn0_db), np.float64)
+    out = np.zeros((len(pts), 11), np.float64)
+    check(lib.ldpcb_run_sweep_multi(g.handle, s.handle, _vp(dev), len(dev), _vp(pts), len(pts), iter_limit,
+                                    max_frames, min_frame_errors, channel_seed, wave_frames, _vp(out)),
+          "run_sweep_multi")
+    return _sweep_records(out)
 
 
 @dataclass

@@ -12,6 +12,9 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
+#include <vector>
+#include <exception>
 
 #include "host.hpp"
 #include "kernels.cuh"
@@ -95,6 +98,9 @@ struct CodeImpl {
     Dev x;
     x.cols = upload(host.cols);
     x.ptrs = {x.cols};
+    // a pageable cudaMemcpy may return before its DMA lands, and decodes run
+    // on non-blocking streams that do not order after the legacy stream
+    cuda_check(cudaDeviceSynchronize(), "table upload");
     return dev.emplace(d, std::move(x)).first->second;
   }
 };
@@ -133,6 +139,11 @@ struct SchedImpl {
     x.vn_pos = upload(tables.vn_pos);
     x.ptrs = {x.cn_off,     x.cn_rec,     x.fix_off, x.fix_rec,   x.fix_rec16, x.tot_rec16,
               x.all_vn_rec, x.tot_vn_rec, x.all_rec, x.edge_slot, x.vn_pos};
+    // The record tables are immutable once uploaded: the streamed kernels
+    // read them before griddepcontrol.wait (stream.cu). Wait for the DMA of
+    // the pageable copies here, since decodes run on non-blocking streams
+    // that are not ordered after the legacy stream.
+    cuda_check(cudaDeviceSynchronize(), "table upload");
     return dev.emplace(d, std::move(x)).first->second;
   }
 };
@@ -586,8 +597,7 @@ int ldpcb_decode_host(ldpcb_code code, ldpcb_schedule s, int64_t frames, const f
                                    : std::max<int64_t>(p0.fpc, (int64_t{32} << 20) / (4 * n));
     chunk = std::min<int64_t>(chunk, frames);
     if (p0.kernel != 2) chunk = (chunk + p0.fpc - 1) / p0.fpc * p0.fpc;  // whole CTAs (streamed: fpc = chunk)
-    const int kSlots = 2;
-    cudaStream_t st[kSlots];
+    constexpr int kSlots = 2;
     struct Buf {
       float* llr = nullptr;
       uint8_t* bits = nullptr;
@@ -596,7 +606,26 @@ int ldpcb_decode_host(ldpcb_code code, ldpcb_schedule s, int64_t frames, const f
       float* post = nullptr;
       int32_t* trace = nullptr;
       int64_t* cnt = nullptr;
-    } buf[kSlots];
+    };
+    // Owns the per-slot device buffers: on every exit (an error thrown by a
+    // copy or a launch included) the buffers are released on their streams
+    // and both streams drained, so nothing stays queued against host memory
+    // the caller may free once this call returns.
+    struct Slots {
+      cudaStream_t st[kSlots] = {};
+      Buf buf[kSlots];
+      ~Slots() {
+        for (int k = 0; k < kSlots; ++k) {
+          if (!st[k]) continue;
+          void* ptrs[] = {buf[k].llr, buf[k].bits, buf[k].it, buf[k].cv, buf[k].post, buf[k].trace, buf[k].cnt};
+          for (void* q : ptrs)
+            if (q) cudaFreeAsync(q, st[k]);  // errors ignored: best effort on the unwind path
+          cudaStreamSynchronize(st[k]);
+        }
+      }
+    } slots;
+    cudaStream_t* st = slots.st;
+    Buf* buf = slots.buf;
     for (int k = 0; k < kSlots; ++k) {
       st[k] = host_stream(k);
       cuda_check(cudaMallocAsync(&buf[k].llr, chunk * n * sizeof(float), st[k]), "cudaMallocAsync");
@@ -653,13 +682,6 @@ int ldpcb_decode_host(ldpcb_code code, ldpcb_schedule s, int64_t frames, const f
         cuda_check(cudaStreamSynchronize(st[k]), "sync");
         for (int i = 0; i < 6; ++i) total[i] += h[i];
       }
-      cudaFreeAsync(buf[k].llr, st[k]);
-      if (buf[k].bits) cudaFreeAsync(buf[k].bits, st[k]);
-      if (buf[k].it) cudaFreeAsync(buf[k].it, st[k]);
-      if (buf[k].cv) cudaFreeAsync(buf[k].cv, st[k]);
-      if (buf[k].post) cudaFreeAsync(buf[k].post, st[k]);
-      if (buf[k].trace) cudaFreeAsync(buf[k].trace, st[k]);
-      if (buf[k].cnt) cudaFreeAsync(buf[k].cnt, st[k]);
       cuda_check(cudaStreamSynchronize(st[k]), "sync");
     }
     if (counters)
@@ -728,87 +750,176 @@ int ldpcb_simulate_frames_device(ldpcb_code code, ldpcb_schedule s, double sigma
   });
 }
 
-// run_sweep (sim.hpp:96-186) on the device: waves of frames, per-frame
-// outcomes copied back, and the point stops at the smallest frame index whose
-// prefix holds min_frame_errors frame errors (or at max_frames). The result
-// does not depend on the wave size, as in the reference.
+}  // extern "C"
+
+namespace {
+
+// Runs fn(i) for i < n_devices, one host thread per entry of `devices`, each
+// bound to its device (the reference's worker pool, sim.hpp:136-150, with a
+// GPU per worker). The first failure is rethrown on the calling thread with
+// its own exception type, after every worker has finished.
+template <class F>
+void on_devices(const int* devices, int n_devices, F&& fn) {
+  need(devices != nullptr && n_devices >= 1, "need at least one device");
+  int count = 0;
+  cuda_check(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+  for (int i = 0; i < n_devices; ++i) need(devices[i] >= 0 && devices[i] < count, "device index out of range");
+  std::vector<std::exception_ptr> errs(n_devices);
+  std::vector<std::thread> pool;
+  pool.reserve(n_devices);
+  for (int i = 0; i < n_devices; ++i)
+    pool.emplace_back([&, i] {
+      try {
+        cuda_check(cudaSetDevice(devices[i]), "cudaSetDevice");
+        fn(i);
+      } catch (...) {
+        errs[i] = std::current_exception();
+      }
+    });
+  for (auto& t : pool) t.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
+
+// run_sweep (sim.hpp:96-186) on one or more GPUs: waves of frames, each wave
+// split into contiguous frame-id ranges over the devices (sim.py shard), the
+// per-frame outcomes copied back in frame order, and the point stops at the
+// smallest frame index whose prefix holds min_frame_errors frame errors (or
+// at max_frames). Frames are keyed by id, so the result depends neither on
+// the wave size nor on the number of devices, as in the reference.
+void run_sweep_impl(ldpcb_code code, ldpcb_schedule s, const int* devices, int n_devices, const double* ebn0_db,
+                    int n_points, int iter_limit, int64_t max_frames, int min_frame_errors, uint64_t channel_seed,
+                    int64_t wave_frames, double* out) {
+  check_pair(code, s);
+  need(ebn0_db != nullptr && n_points >= 1, "need at least one Eb/N0 point");
+  need(min_frame_errors >= 1, "min_frame_errors must be >= 1");
+  need(max_frames >= 1, "max_frames must be >= 1");
+  need(iter_limit >= 1, "max_iters must be >= 1");
+  need(out != nullptr, "null output");
+  const auto& h = code->impl->host;
+  const double rate = static_cast<double>(h.n - h.m) / h.n;
+  int64_t cap = wave_frames > 0 ? wave_frames : (int64_t{1} << 20) * n_devices;
+  cap = std::min(cap, max_frames);
+  std::vector<int32_t> be(cap), it(cap);
+  std::vector<uint8_t> cv(cap);
+  // one wave on every device: worker i decodes [begin + cnt*i/D, begin + cnt*(i+1)/D)
+  auto wave_on_devices = [&](double sigma2, int64_t begin, int64_t cnt) {
+    on_devices(devices, n_devices, [&](int i) {
+      const int64_t lo = cnt * i / n_devices, len = cnt * (i + 1) / n_devices - lo;
+      if (len == 0) return;
+      cudaStream_t st = host_stream(0);
+      int32_t *d_be = nullptr, *d_it = nullptr;
+      uint8_t* d_cv = nullptr;
+      auto cleanup = [&] {
+        if (d_be) cudaFreeAsync(d_be, st);
+        if (d_it) cudaFreeAsync(d_it, st);
+        if (d_cv) cudaFreeAsync(d_cv, st);
+        cudaStreamSynchronize(st);
+      };
+      try {
+        cuda_check(cudaMallocAsync(&d_be, len * 4, st), "cudaMallocAsync");
+        cuda_check(cudaMallocAsync(&d_it, len * 4, st), "cudaMallocAsync");
+        cuda_check(cudaMallocAsync(&d_cv, len, st), "cudaMallocAsync");
+        simulate_frames(code, s, sigma2, channel_seed, begin + lo, len, iter_limit, 1, d_be, d_it, d_cv, nullptr, st);
+        cuda_check(cudaMemcpyAsync(be.data() + lo, d_be, len * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_check(cudaMemcpyAsync(it.data() + lo, d_it, len * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_check(cudaMemcpyAsync(cv.data() + lo, d_cv, len, cudaMemcpyDeviceToHost, st), "D2H");
+        cuda_check(cudaStreamSynchronize(st), "sync");
+      } catch (...) {
+        cleanup();
+        throw;
+      }
+      cleanup();
+    });
+  };
+  for (int pt = 0; pt < n_points; ++pt) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const double sigma2 = ldpcb::awgn_sigma2(ebn0_db[pt], rate);
+    int64_t produced = 0, stop = -1, fe_total = 0, conv = 0;
+    long long bit_errors = 0, iter_sum = 0, iter_conv = 0;
+    // the first wave is small so that high-FER points stop early
+    int64_t wave = std::min<int64_t>(cap, 4096);
+    while (stop < 0) {
+      const int64_t cnt = std::min(wave, max_frames - produced);
+      wave_on_devices(sigma2, produced, cnt);
+      for (int64_t i = 0; i < cnt; ++i) {  // prefix scan (sim.hpp:150-158) + aggregation (:162-181)
+        bit_errors += be[i];
+        fe_total += be[i] > 0;
+        conv += cv[i];
+        iter_sum += it[i];
+        iter_conv += cv[i] ? it[i] : 0;
+        if (fe_total >= min_frame_errors) {
+          stop = produced + i;
+          break;
+        }
+      }
+      produced += cnt;
+      if (stop < 0 && produced >= max_frames) stop = max_frames - 1;
+      wave = std::min(cap, 2 * wave);
+    }
+    const double frames = static_cast<double>(stop + 1);
+    double* o = out + 11 * pt;
+    o[0] = frames;
+    o[1] = static_cast<double>(bit_errors);
+    o[2] = static_cast<double>(fe_total);
+    o[3] = static_cast<double>(conv);
+    o[4] = static_cast<double>(bit_errors) / (frames * h.n);
+    o[5] = static_cast<double>(fe_total) / frames;
+    o[6] = conv > 0 ? static_cast<double>(iter_conv) / conv : 0.0;
+    o[7] = static_cast<double>(iter_sum) / frames;
+    o[8] = iter_limit;
+    o[9] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    o[10] = ebn0_db[pt];
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
 int ldpcb_run_sweep_host(ldpcb_code code, ldpcb_schedule s, const double* ebn0_db, int n_points, int iter_limit,
                          int64_t max_frames, int min_frame_errors, uint64_t channel_seed, int64_t wave_frames,
                          double* out) {
   return guard([&] {
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    run_sweep_impl(code, s, &dev, 1, ebn0_db, n_points, iter_limit, max_frames, min_frame_errors, channel_seed,
+                   wave_frames, out);
+    return LDPCB_OK;
+  });
+}
+
+int ldpcb_run_sweep_multi(ldpcb_code code, ldpcb_schedule s, const int* devices, int n_devices,
+                          const double* ebn0_db, int n_points, int iter_limit, int64_t max_frames,
+                          int min_frame_errors, uint64_t channel_seed, int64_t wave_frames, double* out) {
+  return guard([&] {
+    run_sweep_impl(code, s, devices, n_devices, ebn0_db, n_points, iter_limit, max_frames, min_frame_errors,
+                   channel_seed, wave_frames, out);
+    return LDPCB_OK;
+  });
+}
+
+int ldpcb_simulate_multi(ldpcb_code code, ldpcb_schedule s, const int* devices, int n_devices, double sigma2,
+                         uint64_t channel_seed, int64_t frame_begin, int64_t frames, int max_iters, int early_stop,
+                         int64_t* counters) {
+  return guard([&] {
     check_pair(code, s);
-    need(ebn0_db != nullptr && n_points >= 1, "need at least one Eb/N0 point");
-    need(min_frame_errors >= 1, "min_frame_errors must be >= 1");
-    need(max_frames >= 1, "max_frames must be >= 1");
-    need(iter_limit >= 1, "max_iters must be >= 1");
-    need(out != nullptr, "null output");
-    const auto& h = code->impl->host;
-    const double rate = static_cast<double>(h.n - h.m) / h.n;
-    int64_t cap = wave_frames > 0 ? wave_frames : (int64_t{1} << 20);
-    cap = std::min(cap, max_frames);
-    cudaStream_t st = host_stream(0);
-    int32_t *d_be = nullptr, *d_it = nullptr;
-    uint8_t* d_cv = nullptr;
-    std::vector<int32_t> be(cap), it(cap);
-    std::vector<uint8_t> cv(cap);
-    auto cleanup = [&] {
-      if (d_be) cudaFreeAsync(d_be, st);
-      if (d_it) cudaFreeAsync(d_it, st);
-      if (d_cv) cudaFreeAsync(d_cv, st);
-      cudaStreamSynchronize(st);
-    };
-    try {
-      cuda_check(cudaMallocAsync(&d_be, cap * 4, st), "cudaMallocAsync");
-      cuda_check(cudaMallocAsync(&d_it, cap * 4, st), "cudaMallocAsync");
-      cuda_check(cudaMallocAsync(&d_cv, cap, st), "cudaMallocAsync");
-      for (int pt = 0; pt < n_points; ++pt) {
-        const auto t0 = std::chrono::steady_clock::now();
-        const double sigma2 = ldpcb::awgn_sigma2(ebn0_db[pt], rate);
-        int64_t produced = 0, stop = -1, fe_total = 0, conv = 0;
-        long long bit_errors = 0, iter_sum = 0, iter_conv = 0;
-        // the first wave is small so that high-FER points stop early
-        int64_t wave = std::min<int64_t>(cap, 4096);
-        while (stop < 0) {
-          const int64_t cnt = std::min(wave, max_frames - produced);
-          simulate_frames(code, s, sigma2, channel_seed, produced, cnt, iter_limit, 1, d_be, d_it, d_cv, nullptr, st);
-          cuda_check(cudaMemcpyAsync(be.data(), d_be, cnt * 4, cudaMemcpyDeviceToHost, st), "D2H");
-          cuda_check(cudaMemcpyAsync(it.data(), d_it, cnt * 4, cudaMemcpyDeviceToHost, st), "D2H");
-          cuda_check(cudaMemcpyAsync(cv.data(), d_cv, cnt, cudaMemcpyDeviceToHost, st), "D2H");
-          cuda_check(cudaStreamSynchronize(st), "sync");
-          for (int64_t i = 0; i < cnt; ++i) {  // prefix scan (sim.hpp:150-158) + aggregation (:162-181)
-            bit_errors += be[i];
-            fe_total += be[i] > 0;
-            conv += cv[i];
-            iter_sum += it[i];
-            iter_conv += cv[i] ? it[i] : 0;
-            if (fe_total >= min_frame_errors) {
-              stop = produced + i;
-              break;
-            }
-          }
-          produced += cnt;
-          if (stop < 0 && produced >= max_frames) stop = max_frames - 1;
-          wave = std::min(cap, 2 * wave);
-        }
-        const double frames = static_cast<double>(stop + 1);
-        double* o = out + 11 * pt;
-        o[0] = frames;
-        o[1] = static_cast<double>(bit_errors);
-        o[2] = static_cast<double>(fe_total);
-        o[3] = static_cast<double>(conv);
-        o[4] = static_cast<double>(bit_errors) / (frames * h.n);
-        o[5] = static_cast<double>(fe_total) / frames;
-        o[6] = conv > 0 ? static_cast<double>(iter_conv) / conv : 0.0;
-        o[7] = static_cast<double>(iter_sum) / frames;
-        o[8] = iter_limit;
-        o[9] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-        o[10] = ebn0_db[pt];
-      }
-    } catch (...) {
-      cleanup();
-      throw;
-    }
-    cleanup();
+    need(counters != nullptr, "null counters");
+    need(frames >= 0 && frame_begin >= 0, "bad frame range");
+    need(devices != nullptr && n_devices >= 1, "need at least one device");
+    // per-worker counters, summed on the host once every worker is done (the
+    // in-process counterpart of the NCCL allreduce of sim.py / bench.py)
+    std::vector<std::array<int64_t, 6>> part(n_devices);
+    on_devices(devices, n_devices, [&](int i) {
+      part[i].fill(0);
+      const int64_t lo = frames * i / n_devices, len = frames * (i + 1) / n_devices - lo;
+      if (len == 0) return;
+      if (ldpcb_simulate_host(code, s, sigma2, channel_seed, frame_begin + lo, len, max_iters, early_stop,
+                              part[i].data()) != LDPCB_OK)
+        throw std::runtime_error("device " + std::to_string(devices[i]) + ": " + g_last_error);
+    });
+    for (const auto& c : part)
+      for (int k = 0; k < 6; ++k) counters[k] += c[k];
     return LDPCB_OK;
   });
 }

@@ -138,6 +138,21 @@ static void gpu_cases() {
   }
   CHECK(res[1].frames > res[0].frames);
   CHECK_THROWS_AS(run_sweep(c1, pf, {}, 20, 10, 1), std::invalid_argument);
+
+  // several GPUs through the boundary (the north-star split, sim.hpp:96-186
+  // driven from C++): device 0 listed twice = two workers with contiguous
+  // frame ranges; counters and sweep records equal the one-device results
+  const auto sim2 = simulate(c1, nd, 2.0, 1, 0, 1000, 20, true, {0, 0});
+  CHECK(sim2 == sim);
+  const auto res2 = run_sweep(c1, pf, {1.5, 2.0}, 20, 100000, 25, 1, {0, 0, 0});
+  CHECK(res2.size() == res.size());
+  for (std::size_t i = 0; i < res.size() && i < res2.size(); ++i) {
+    CHECK(res2[i].frames == res[i].frames && res2[i].bit_errors == res[i].bit_errors);
+    CHECK(res2[i].frame_errors == res[i].frame_errors && res2[i].converged_frames == res[i].converged_frames);
+    CHECK(res2[i].mean_iters_all == res[i].mean_iters_all);
+  }
+  CHECK_THROWS_AS(simulate(c1, nd, 2.0, 1, 0, 10, 20, true, {}), std::invalid_argument);
+  CHECK_THROWS_AS(simulate(c1, nd, 2.0, 1, 0, 10, 20, true, {0, 4096}), std::invalid_argument);
   CHECK_THROWS_AS(make_per_frame_schedule(c1, ScheduleKind::nondisjoint, 8, 0.9, 2), std::invalid_argument);
 }
 

@@ -403,24 +403,39 @@ def streamed(P):
     P.set_kernel(0)
 
 
-@pytest.mark.parametrize("sched", ["ndgsbp", "gsbp", "bp"])
-def test_streamed_equals_resident(P, torch, orc, sched):
+@pytest.mark.parametrize("case", ["c1_nd", "c1_gs", "c1_bp", "c3_nd", "irregular"])
+@pytest.mark.parametrize("pdl", ["1", "0"])
+def test_streamed_equals_resident(P, torch, orc, case, pdl):
     """Same arithmetic in the same order: the streamed kernels reproduce the
-    resident kernel bit for bit (C1 code, ragged frame count)."""
-    g = P.configs.c1_code()
-    s = P.configs.c1_schedules(g)[sched]
-    llr = cu(torch, orc.transmit_batch_f32(P.sigma2_from_ebn0(1.75, g.rate), 6, g.n_vars, 0, 301, THREADS))
-    for es, iters in ((True, 20), (False, 10)):
-        P.set_kernel(1)
-        a = to_np(P.decode_batch(g, s, llr, iters, early_stop=es, posterior=True, trace=True))
-        P.set_kernel(2)
-        try:
-            assert P.plan(g, s, 301)["kernel"] == 2
+    resident kernel bit for bit (ragged frame count), on check-regular rows
+    (C1, packed records) and on irregular rows (C3 QC code and a {2,3,8}
+    ensemble: degree buckets 8/16, odd per-CN slot counts), with and without
+    programmatic dependent launch (its record loads precede the wait)."""
+    if case.startswith("c1"):
+        g = P.configs.c1_code()
+        s = P.configs.c1_schedules(g)[{"c1_nd": "ndgsbp", "c1_gs": "gsbp", "c1_bp": "bp"}[case]]
+    elif case == "c3_nd":
+        g = P.configs.c3_code()
+        s = P.configs.c3_schedules(g)["ndgsbp"]
+    else:
+        g = P.TannerGraph.irregular(2400, [2, 3, 8], [1200, 960, 240], 6, 5)
+        s = P.GroupSchedule.windows(g, 5, 300, 240)
+    F = 301
+    llr = cu(torch, orc.transmit_batch_f32(P.sigma2_from_ebn0(1.75, g.rate), 6, g.n_vars, 0, F, THREADS))
+    os.environ["LDPCB_STREAM_PDL"] = pdl
+    try:
+        for es, iters in ((True, 20), (False, 10)):
+            P.set_kernel(1)
+            a = to_np(P.decode_batch(g, s, llr, iters, early_stop=es, posterior=True, trace=True))
+            P.set_kernel(2)
+            assert P.plan(g, s, F)["kernel"] == 2
             b = to_np(P.decode_batch(g, s, llr, iters, early_stop=es, posterior=True, trace=True))
-        finally:
             P.set_kernel(0)
-        for k in a:
-            assert np.array_equal(a[k], b[k]), (sched, es, k)
+            for k in a:
+                assert np.array_equal(a[k], b[k]), (case, es, k)
+    finally:
+        P.set_kernel(0)
+        os.environ.pop("LDPCB_STREAM_PDL", None)
 
 
 def test_streamed_messages_and_packed_bits(P, torch, orc, streamed):
@@ -438,25 +453,69 @@ def test_streamed_messages_and_packed_bits(P, torch, orc, streamed):
     assert np.array_equal(np.packbits(b["bits"], axis=1, bitorder="little"), a["bits"])
 
 
-def test_c4_long_code_parity(P, torch, orc):
+@pytest.mark.parametrize("es,iters", [(False, 10), (True, 30)])
+def test_c4_long_code_parity(P, torch, orc, es, iters):
     """BASELINE config 4 code (n=64800, VN degrees {2,3,8}, 45 windows of 960
-    at stride 720) at 1.1 dB: decoded by the HBM-streamed kernel."""
+    at stride 720) at 1.1 dB, decoded by the HBM-streamed kernels with the
+    library defaults: C5-long's fixed 10 iterations (lazy totals, no trace:
+    the benchmarked mode) and config 4's <= 30 iterations with early stop.
+    2000 frames against the reference decoder at the full 99.9 % bar."""
     g = P.configs.c4_code()
     s = P.configs.c4_schedules(g)["ndgsbp"]
     assert P.plan(g, s, 64)["kernel"] == 2
     og = orc.graph(g.n_vars, *g.csr())
     s2 = P.sigma2_from_ebn0(1.1, g.rate)
-    F = 24
+    F = 2000
     llr = orc.transmit_batch_f32(s2, 1, g.n_vars, 0, F, THREADS)
-    for es, iters in ((False, 10), (True, 30)):
-        gpu = to_np(P.decode_batch(g, s, cu(torch, llr), iters, early_stop=es, posterior=True))
-        ref = orc.decode_batch(og, s.groups, llr, iters, early_stop=es, threads=THREADS, posterior=True)
-        same = frame_parity(gpu, ref)
-        frac, worst = post_stats(gpu["posterior"], ref["posterior"], same & (ref["converged"] == 1))
-        print(f"C4 es={es}: identical {same.mean():.4f}, conv {ref['converged'].mean():.3f}, "
-              f"posteriors within 1e-3 {frac:.6f} (max {worst:.2e})")
-        assert same.mean() >= (1.0 if not es else 0.95)
-        assert frac >= 0.9999
+    gpu = to_np(P.decode_batch(g, s, cu(torch, llr), iters, early_stop=es, packed=False, posterior=True))
+    ref = orc.decode_batch(og, s.groups, llr, iters, early_stop=es, threads=THREADS, posterior=True)
+    same = frame_parity(gpu, ref)
+    frac, worst = post_stats(gpu["posterior"], ref["posterior"], same & (ref["converged"] == 1))
+    print(f"C4 es={es} <= {iters} it, {F} frames: identical {same.mean():.5f}, conv {ref['converged'].mean():.3f}, "
+          f"iters {gpu['iterations'].mean():.2f}/{ref['iterations'].mean():.2f}, posteriors within 1e-3 "
+          f"{frac:.6f} (max {worst:.2e})")
+    assert same.mean() >= 0.999
+    assert frac >= 0.9999
+
+
+@pytest.mark.parametrize("sched", ["ndgsbp", "gsbp", "bp"])
+def test_c5_benchmarked_mode_parity(P, torch, orc, sched):
+    """The exact mode bench.py measures: C1 code at 2.0 dB, fixed 10
+    iterations, no early stop, no trace, library defaults (lazy totals: the
+    exact posterior re-sum runs only in the last iteration, decoder.cu), packed
+    bits and counters, 10^4 frames against the reference's fixed-iteration
+    composition (init_state + run_subiteration, oracle/ref_driver.cpp)."""
+    g = P.configs.c1_code()
+    s = P.configs.c1_schedules(g)[sched]
+    og = orc.graph(g.n_vars, *g.csr())
+    F = 10_000
+    llr = orc.transmit_batch_f32(P.sigma2_from_ebn0(2.0, g.rate), 1, g.n_vars, 0, F, THREADS)
+    x = cu(torch, llr)
+    ref = orc.decode_batch(og, s.groups, llr, 10, early_stop=False, threads=THREADS, posterior=True)
+    P.set_lazy_totals(True)  # the library default
+    cnt = torch.zeros(6, dtype=torch.int64, device="cuda")
+    gpu = to_np(P.decode_batch(g, s, x, 10, early_stop=False, packed=True, counters=cnt))
+    post = to_np(P.decode_batch(g, s, x, 10, early_stop=False, packed=True, posterior=True))
+    assert np.array_equal(gpu["bits"], post["bits"])  # requesting posteriors changes nothing
+    gpu["bits"] = np.unpackbits(gpu["bits"], axis=1, count=g.n_vars, bitorder="little")
+    same = frame_parity(gpu, ref)
+    frac, worst = post_stats(post["posterior"], ref["posterior"], same & (ref["converged"] == 1))
+    be = gpu["bits"].sum(1)
+    conv = int(gpu["converged"].sum())
+    assert cnt.cpu().tolist() == [F, int(be.sum()), int((be > 0).sum()), conv, 10 * F, 10 * conv]
+    # the same decode with the exact re-sum in every iteration
+    P.set_lazy_totals(False)
+    try:
+        exact = to_np(P.decode_batch(g, s, x, 10, early_stop=False, packed=False))
+    finally:
+        P.set_lazy_totals(True)
+    same_exact = frame_parity(exact, ref)
+    lazy_vs_exact = frame_parity(gpu, exact).mean()
+    print(f"C5 {sched} fixed 10 it, lazy totals: identical {same.mean():.5f} (exact totals every iteration "
+          f"{same_exact.mean():.5f}; lazy vs exact {lazy_vs_exact:.5f}), posteriors within 1e-3 {frac:.6f} "
+          f"(max {worst:.2e}), FER {(be > 0).mean():.4f} / ref {(ref['bits'].sum(1) > 0).mean():.4f}")
+    assert same.mean() >= 0.999 and same_exact.mean() >= 0.999 and lazy_vs_exact >= 0.999
+    assert frac >= 0.9999
 
 
 @pytest.mark.parametrize("case", ["c1_nd", "c1_gs", "c1_bp", "irregular", "c3_nd"])

@@ -235,3 +235,52 @@ def test_channel_stream_jump_ahead_matches_stepping(P):
             out = (C.c_uint64 * 4)()
             assert lib.ldpcb_channel_stream_state(seed, frame, d, out) == 0
             assert list(out) == w, (seed, frame, d)
+
+
+def test_decode_host_rejects_bad_host_buffers(P):
+    """decode_host passes raw host pointers to ldpcb_decode_host, which reads
+    fp32 LLRs and D2H-copies outputs of exact sizes: wrong dtypes, shapes
+    or sizes are refused before the library is called (no GPU needed)."""
+    g = P.TannerGraph.random_regular(60, 3, 6, 21)
+    s = P.make_flooding_schedule(g)
+    F = 4
+    ok = np.zeros((F, 60), np.float32)
+    with pytest.raises(ValueError, match="float32"):
+        P.decode_host(g, s, np.zeros((F, 60)), 5)  # float64: the reference decoder's own LLR type
+    with pytest.raises(ValueError, match="code length"):
+        P.decode_host(g, s, np.zeros((F, 59), np.float32), 5)
+    with pytest.raises(ValueError, match="contiguous"):
+        P.decode_host(g, s, np.zeros((60, F), np.float32).T, 5)
+    with pytest.raises(ValueError, match="bits"):
+        P.decode_host(g, s, ok, 5, packed=True, bits=np.zeros((F, 60), np.uint8))  # unpacked size, packed layout
+    with pytest.raises(ValueError, match="bits"):
+        P.decode_host(g, s, ok, 5, packed=False, bits=np.zeros((F, 8), np.uint8))
+    with pytest.raises(ValueError, match="posterior"):
+        P.decode_host(g, s, ok, 5, posterior=np.zeros((F, 59), np.float32))
+    with pytest.raises(ValueError, match="syndrome_trace"):
+        P.decode_host(g, s, ok, 5, syndrome_trace=np.zeros((F, 4), np.int32))
+    with pytest.raises(ValueError, match="iterations"):
+        P.decode_host(g, s, ok, 5, iterations=np.zeros(F, np.int64))
+    with pytest.raises(ValueError, match="converged"):
+        P.decode_host(g, s, ok, 5, converged=np.zeros(F + 1, np.uint8))
+    with pytest.raises(ValueError, match="counters"):
+        P.decode_host(g, s, ok, 5, counters=np.zeros(6, np.int32))
+    import torch
+
+    with pytest.raises(ValueError, match="counters"):
+        P.decode_batch(g, s, torch.zeros((F, 60)), 5, counters=torch.zeros(6, dtype=torch.int64))
+
+
+def test_bench_fixture_matches_the_product_constructions(P):
+    """bench.py's reference arm reads the C5 codes and windows from
+    bench_fixtures/c5_workloads.npz (so that process never loads the
+    product): the frozen arrays must be the ones the product builds."""
+    z = np.load(os.path.join(os.path.dirname(GOLDEN), "..", "bench_fixtures", "c5_workloads.npz"))
+    for key, g, s in (("c5_n1008", P.configs.c1_code(), "c1"), ("c5_n64800", P.configs.c4_code(), "c4")):
+        sch = (P.configs.c1_schedules(g) if s == "c1" else P.configs.c4_schedules(g))["ndgsbp"]
+        off, cols = g.csr()
+        assert int(z[f"{key}_n"]) == g.n_vars
+        assert np.array_equal(z[f"{key}_row_off"], off) and np.array_equal(z[f"{key}_cols"], cols)
+        flat = [c for grp in sch.groups for c in grp]
+        assert np.array_equal(z[f"{key}_grp_cns"], flat)
+        assert int(z[f"{key}_edge_updates_per_iter"]) == sch.edge_updates_per_iter
