@@ -180,9 +180,12 @@ class CpuReference:
         return max(self.threads, int(cal * seconds / max(dt, 1e-6)))
 
     def baseline(self, seconds):
-        """One timed sample of about `seconds` -> cpu_baseline dict."""
-        frames = self.frames_for(seconds)
-        dt = self.run(frames)
+        """Timed samples until at least `seconds` of decoding -> cpu_baseline dict."""
+        per = self.frames_for(seconds / 3)
+        frames, dt = 0, 0.0
+        while dt < seconds:
+            dt += self.run(per)
+            frames += per
         return {"value": frames * self.K / dt, "unit": UNIT, "cores": self.threads, "kind": self.orc.kind,
                 "sample": f"{frames} frames of the same workload, {self.iters} fixed iterations ({dt:.1f} s, "
                           f"{self.threads} threads)"}
@@ -191,7 +194,7 @@ class CpuReference:
 def reference_leg(args, name):
     ref = CpuReference(name, args.iters)
     per_step = max(args.cpu_seconds / max(args.steps, 1), 1.0)
-    frames = ref.frames_for(per_step)
+    frames = int(ref.frames_for(per_step) * 1.15)  # the timed steps together exceed --cpu-seconds
     warm = max(ref.threads, frames // 4)
     for _ in range(args.warmup):
         ref.run(warm)

@@ -112,6 +112,7 @@ struct SchedImpl {
   std::mutex mu;
   struct Dev {
     int32_t *cn_off, *cn_rec, *fix_off, *fix_rec, *fix_rec16, *tot_rec16, *all_vn_rec, *tot_vn_rec, *all_rec, *edge_slot, *vn_pos;
+    uint32_t *cn_fresh, *fix_fresh;
     std::vector<void*> ptrs;
   };
   std::map<int, Dev> dev;
@@ -137,8 +138,10 @@ struct SchedImpl {
     x.all_rec = upload(tables.all_rec);
     x.edge_slot = upload(tables.edge_slot);
     x.vn_pos = upload(tables.vn_pos);
+    x.cn_fresh = upload(tables.cn_fresh);
+    x.fix_fresh = upload(tables.fix_fresh);
     x.ptrs = {x.cn_off,     x.cn_rec,     x.fix_off, x.fix_rec,   x.fix_rec16, x.tot_rec16,
-              x.all_vn_rec, x.tot_vn_rec, x.all_rec, x.edge_slot, x.vn_pos};
+              x.all_vn_rec, x.tot_vn_rec, x.all_rec, x.edge_slot, x.vn_pos,  x.cn_fresh, x.fix_fresh};
     // The record tables are immutable once uploaded: the streamed kernels
     // read them before griddepcontrol.wait (stream.cu). Wait for the DMA of
     // the pageable copies here, since decodes run on non-blocking streams
@@ -273,6 +276,9 @@ ldpcb::DevGraph dev_graph(ldpcb_code code, ldpcb_schedule s) {
   g.all_vn_rec = d.all_vn_rec;
   g.tot_vn_rec = d.tot_vn_rec;
   g.all_rec = d.all_rec;
+  g.cn_fresh = d.cn_fresh;
+  g.fix_fresh = d.fix_fresh;
+  g.covers = t.covers;
   const auto& sh = s->impl->host;
   g.per_frame = sh.per_frame;
   g.regroup = sh.regroup;

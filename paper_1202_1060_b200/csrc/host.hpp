@@ -127,6 +127,19 @@ struct KernelTables {
   // every record holds positions, not VN ids (bank colouring relabels VNs)
   std::vector<int32_t> vn_pos;
   int max_cn_items = 0, max_fix_items = 0;
+  // Fresh frames (HBM-streamed frame queue, stream.cu): a lane refilled with a
+  // new frame at an iteration boundary keeps the previous frame's c2v and
+  // posteriors; during its first iteration the kernels read the values that
+  // zero c2v and P = L would give, from static per-record bits:
+  //   cn_fresh[i]  (per cn_rec record) bit 31: first processing of the CN in
+  //                iteration order (its old c2v counts as 0); bit k: the VN at
+  //                position k is touched by no earlier group (read L, not P)
+  //   fix_fresh[i] (per fix_rec record) bit j: slot field j (0 = first slot)
+  //                belongs to a CN processed in this group or an earlier one
+  // covers: every CN is in some group and every VN is touched (the first
+  // iteration then leaves no stale value behind).
+  std::vector<uint32_t> cn_fresh, fix_fresh;
+  bool covers = false;
 };
 
 // cs = CN record stride in ints (>= 2 + max CN degree, multiple of 4)

@@ -517,9 +517,21 @@ KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, boo
   t.fix_off.assign(1, 0);
   std::vector<int> touches(c.n, 0);
   std::vector<int> shared_vns;
+  std::vector<char> processed(c.m, 0), touched(c.n, 0);  // fresh-frame bookkeeping (host.hpp)
   for (int g = 0; g < s.G; ++g) {
     const auto& cns = group_cns[g];
     for (int r : cns) t.recompute |= put_cn(t.cn_rec, r, &single[g]) != 0;
+    for (int r : cns) {  // against the state before this group (Jacobi)
+      const int off = c.row_off[r], deg = c.row_off[r + 1] - off;
+      uint32_t f = processed[r] ? 0u : 1u << 31;
+      for (int p = 0; p < deg && p < 31; ++p)
+        if (!touched[c.cols[off + perm[off + p]]]) f |= 1u << p;
+      t.cn_fresh.push_back(f);
+    }
+    for (int r : cns) {
+      processed[r] = 1;
+      for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e) touched[c.cols[e]] = 1;
+    }
     for (int r : cns)
       for (int e = c.row_off[r]; e < c.row_off[r + 1]; ++e) ++touches[c.cols[e]];
     shared_vns.clear();
@@ -536,6 +548,12 @@ KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, boo
     std::sort(shared_vns.begin(), shared_vns.end());
     if (c.max_vdeg < 16) order_by_degree(shared_vns, 0x66697875ull + g);
     for (int v : shared_vns) put_vn(t.fix_rec, v);
+    for (int v : shared_vns) {  // slot fields of CNs processed by the end of this group
+      uint32_t f = 0;
+      for (int j = c.var_off[v]; j < c.var_off[v + 1] && j - c.var_off[v] < 32; ++j)
+        if (processed[c.var_cns[j]]) f |= 1u << (j - c.var_off[v]);
+      t.fix_fresh.push_back(f);
+    }
     if (t.vs16)
       for (int v : shared_vns) put_vn16(t.fix_rec16, v);
     t.cn_off.push_back(t.cn_off.back() + static_cast<int>(cns.size()));
@@ -543,6 +561,9 @@ KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, boo
     t.max_cn_items = std::max(t.max_cn_items, static_cast<int>(cns.size()));
     t.max_fix_items = std::max(t.max_fix_items, static_cast<int>(shared_vns.size()));
   }
+  t.covers = c.max_vdeg <= 31 && c.max_cdeg <= 31 &&
+             std::all_of(processed.begin(), processed.end(), [](char x) { return x != 0; }) &&
+             std::all_of(touched.begin(), touched.end(), [](char x) { return x != 0; });
   // all_vn_rec is indexed by shared-memory position (the per-frame kernel
   // looks records up by the positions in its CN records)
   std::vector<int> all(c.n);

@@ -29,6 +29,10 @@ struct DevGraph {
   const int32_t* all_vn_rec = nullptr;  // [n] VN records, indexed by VN
   const int32_t* tot_vn_rec = nullptr;  // [n] VN records in bank-coloured order
   const int32_t* all_rec = nullptr;     // [m] CN records, syndrome
+  // fresh-frame bits of the streamed frame queue (host.hpp KernelTables)
+  const uint32_t* cn_fresh = nullptr;   // per cn_rec record
+  const uint32_t* fix_fresh = nullptr;  // per fix_rec record
+  bool covers = false;
   // per-frame random grouping (host.hpp ScheduleData::per_frame)
   bool per_frame = false, regroup = false, balanced = false;
   int nominal = 0, k_overlap = 0, list_slots = 0;

@@ -27,6 +27,12 @@ namespace {
 
 using namespace dev;
 
+// Lane states (done[]): bit 0 set = the lane is not decoding. Chunk mode
+// uses 0 / 1; the frame queue adds 2 = decoding the first iteration of a
+// frame it was refilled with ("fresh", host.hpp KernelTables::cn_fresh) and
+// 3 = retiring (stopped this iteration, outputs pending).
+enum LaneState : int { kLive = 0, kIdle = 1, kFresh = 2, kRetiring = 3 };
+
 struct ChunkState {
   int64_t B = 0;     // layout stride (frames), multiple of 4
   int nb = 0;        // frames of this chunk that are real
@@ -39,6 +45,12 @@ struct ChunkState {
   int* iters = nullptr;   // [B]
   int* conv = nullptr;    // [B]
   int* berr = nullptr;    // [B]
+  // frame queue (launch_stream_queue)
+  int64_t* frame = nullptr;           // [B] frame id held by each lane, -1 idle
+  unsigned* sw = nullptr;             // [n][B/32] hard-decision sign words
+  int* list = nullptr;                // [B] lanes retiring this iteration
+  int* ctl = nullptr;                 // [0] retiring lanes, [1] lanes decoding
+  unsigned long long* next = nullptr; // next frame id to hand out
 };
 
 // Programmatic dependent launch (per-group kernels): a CTA lets the next
@@ -81,18 +93,44 @@ __device__ __forceinline__ void stv(float* p, const Vec<V>& x) {
   else
     *p = x.v[0];
 }
-// done flags of the thread's V frames, bit i = frame i
+// lane states of the thread's V frames
 template <int V>
-__device__ __forceinline__ unsigned done_bits(const ChunkState& s, int64_t q) {
+struct States {
+  int d[V];
+};
+template <int V>
+__device__ __forceinline__ States<V> load_states(const ChunkState& s, int64_t q) {
+  States<V> r;
   if constexpr (V == 4) {
     const int4 d = *reinterpret_cast<const int4*>(s.done + 4 * q);
-    return (d.x != 0) | (d.y != 0) << 1 | (d.z != 0) << 2 | (d.w != 0) << 3;
+    r.d[0] = d.x, r.d[1] = d.y, r.d[2] = d.z, r.d[3] = d.w;
   } else if constexpr (V == 2) {
     const int2 d = *reinterpret_cast<const int2*>(s.done + 2 * q);
-    return (d.x != 0) | (d.y != 0) << 1;
+    r.d[0] = d.x, r.d[1] = d.y;
   } else {
-    return s.done[q] != 0;
+    r.d[0] = s.done[q];
   }
+  return r;
+}
+// bit i set: frame i of the vector is not decoding
+template <int V>
+__device__ __forceinline__ unsigned done_bits(const States<V>& st) {
+  unsigned b = 0;
+#pragma unroll
+  for (int i = 0; i < V; ++i) b |= static_cast<unsigned>(st.d[i] & 1) << i;
+  return b;
+}
+// bit i set: frame i is in the first iteration of a refilled frame
+template <int V>
+__device__ __forceinline__ unsigned fresh_bits(const States<V>& st) {
+  unsigned b = 0;
+#pragma unroll
+  for (int i = 0; i < V; ++i) b |= static_cast<unsigned>(st.d[i] == kFresh) << i;
+  return b;
+}
+template <int V>
+__device__ __forceinline__ unsigned done_bits(const ChunkState& s, int64_t q) {
+  return done_bits<V>(load_states<V>(s, q));
 }
 
 // L = P = clamp(llr) in log2 units, transposed [nb][n] -> [n][B] through a
@@ -126,9 +164,13 @@ __global__ void stream_init(int n, const int32_t* __restrict__ pos, const float*
   }
 }
 
-// CN phase of one group over (record, V-frame vector) items.
+// CN phase of one group over (record, V-frame vector) items. fresh (frame
+// queue only, else null): per-record bits of KernelTables::cn_fresh for lanes
+// in the first iteration of a refilled frame (old c2v = 0, P = L at a VN's
+// first touch), which is what a zeroed c2v and P = L would give.
 template <int D, bool EXACT, int V>
-__global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ recs, int CS, int count, ChunkState s) {
+__global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ recs, int CS, int count, ChunkState s,
+                                                 const uint32_t* __restrict__ fresh) {
   pdl_launch_next();
   const int64_t QB = s.B / V;
   const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -139,8 +181,11 @@ __global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ rec
   // previous kernel, so its latency overlaps that kernel's drain
   const CnRecord<D, EXACT> cr(recs + static_cast<int64_t>(j) * CS, CS);
   pdl_wait();
-  const unsigned dn = done_bits<V>(s, q);
+  const States<V> st = load_states<V>(s, q);
+  const unsigned dn = done_bits<V>(st);
   if (dn == (1u << V) - 1) return;
+  const unsigned fr = fresh ? fresh_bits<V>(st) : 0u;
+  const uint32_t fbits = fr ? __ldg(fresh + j) : 0u;
   const int base = cr.slot();
   const unsigned mask = cr.mask();
   const int deg = cr.deg();
@@ -150,6 +195,12 @@ __global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ rec
     if (cr.has(k)) {
       pv[k] = ldv<V>(s.P + static_cast<int64_t>(cr.var(k)) * s.B + V * q);
       old[k] = ldv<V>(s.c2v + static_cast<int64_t>(base + k) * s.B + V * q);
+      if (fr && (fbits & (1u << k))) {  // first touch of this VN in a fresh frame: P = L
+        const Vec<V> l = ldv<V>(s.L + static_cast<int64_t>(cr.var(k)) * s.B + V * q);
+#pragma unroll
+        for (int i = 0; i < V; ++i)
+          if (fr & (1u << i)) pv[k].v[i] = l.v[i];
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < V; ++i) pv[k].v[i] = old[k].v[i] = 0.f;
@@ -158,27 +209,26 @@ __global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ rec
   Vec<V> out[D];
 #pragma unroll
   for (int i = 0; i < V; ++i) {
+    const bool zero_old = (fr & (1u << i)) && (fbits >> 31);  // first processing of this CN
     float x[D];
 #pragma unroll
-    for (int k = 0; k < D; ++k) x[k] = pv[k].v[i] - old[k].v[i];
+    for (int k = 0; k < D; ++k) x[k] = pv[k].v[i] - (zero_old ? 0.f : old[k].v[i]);
     boxplus_row<D, EXACT>(x, deg, [&](int k, float c) { out[k].v[i] = c; });
   }
-  // frames that already stopped (decoder.hpp:173-177) keep their state
-#pragma unroll
-  for (int i = 0; i < V; ++i)
-    if (dn & (1u << i))
-#pragma unroll
-      for (int k = 0; k < D; ++k) out[k].v[i] = old[k].v[i];
 #pragma unroll
   for (int k = 0; k < D; ++k) {
     if (!cr.has(k)) continue;
-    stv<V>(s.c2v + static_cast<int64_t>(base + k) * s.B + V * q, out[k]);
-    if (mask & (1u << k)) {
-      Vec<V> p;
+    Vec<V> o, p;
 #pragma unroll
-      for (int i = 0; i < V; ++i) p.v[i] = (pv[k].v[i] - old[k].v[i]) + out[k].v[i];
-      stv<V>(s.P + static_cast<int64_t>(cr.var(k)) * s.B + V * q, p);
+    for (int i = 0; i < V; ++i) {
+      const bool zero_old = (fr & (1u << i)) && (fbits >> 31);
+      // frames that already stopped (decoder.hpp:173-177) keep their state
+      const bool live = !(dn & (1u << i));
+      o.v[i] = live ? out[k].v[i] : old[k].v[i];
+      p.v[i] = live ? (pv[k].v[i] - (zero_old ? 0.f : old[k].v[i])) + out[k].v[i] : pv[k].v[i];
     }
+    stv<V>(s.c2v + static_cast<int64_t>(base + k) * s.B + V * q, o);
+    if (mask & (1u << k)) stv<V>(s.P + static_cast<int64_t>(cr.var(k)) * s.B + V * q, p);
   }
 }
 
@@ -188,7 +238,7 @@ __global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ rec
 // stops there (a warp serves one VN, so the exit is warp-uniform).
 template <int V>
 __global__ void __launch_bounds__(256) stream_vnsum(const int4* __restrict__ recs, int vs4, int count, ChunkState s,
-                                                    int skip_done) {
+                                                    int skip_done, const uint32_t* __restrict__ fresh) {
   pdl_launch_next();
   const int64_t QB = s.B / V;
   const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -198,17 +248,25 @@ __global__ void __launch_bounds__(256) stream_vnsum(const int4* __restrict__ rec
   const int4* rec = recs + static_cast<int64_t>(j) * vs4;
   int4 t = __ldg(rec);  // constant table: requested before the wait
   pdl_wait();
-  if (skip_done && done_bits<V>(s, q) == (1u << V) - 1) return;
+  const States<V> st = load_states<V>(s, q);
+  if (skip_done && done_bits<V>(st) == (1u << V) - 1) return;
+  // fresh lanes (frame queue): slot fields of CNs not processed yet in the
+  // frame's first iteration hold the previous frame's c2v and count as 0
+  const unsigned fr = fresh ? fresh_bits<V>(st) : 0u;
+  const uint32_t valid = fr ? __ldg(fresh + j) : ~0u;
   const int v = t.x;
   Vec<V> acc = ldv<V>(s.L + static_cast<int64_t>(v) * s.B + V * q);
+  int field = 0;
   auto add = [&](int slot) {
     const Vec<V> c = ldv<V>(s.c2v + static_cast<int64_t>(slot) * s.B + V * q);
+    const bool stale = !((valid >> field) & 1u);
 #pragma unroll
-    for (int i = 0; i < V; ++i) acc.v[i] += c.v[i];
+    for (int i = 0; i < V; ++i) acc.v[i] += (stale && (fr & (1u << i))) ? 0.f : c.v[i];
   };
   const int zero = s.zero_slot;
   auto add_nz = [&](int slot) {
     if (slot != zero) add(slot);
+    ++field;
   };
   add_nz(t.y);
   add_nz(t.z);
@@ -352,20 +410,228 @@ __global__ void stream_dump(const DevGraph g, ChunkState s, float* c2v_out, floa
     v2c_out[(frame0 + f) * g.E + e] = clamp_bits(s.P[static_cast<int64_t>(__ldg(g.vn_pos + __ldg(g.cols + e))) * s.B + f] - c) * kLn2;
 }
 
+// ---- frame queue (early stop): lanes retire and refill at iteration ends
+//
+// A lane whose frame stops (zero syndrome, decoder.hpp:173-177) or reaches
+// max_iters writes that frame's outputs and takes the next frame id from a
+// counter, as the reference's pool pulls the next frame (sim.hpp:136-150).
+// Only the new frame's channel LLRs are written (L); its stale c2v and
+// posteriors are masked by the fresh bits during its first iteration.
+// Posteriors are kept in place between syndrome tests (no all-VN re-sum per
+// iteration): the hard decision of a posterior within kNearZero of 0 is taken
+// from its exact re-sum (P = L + sum c2v, decoder.hpp:162-166), far outside
+// the rounding the in-place updates can accumulate (< 1e-2 in log2 units over
+// hundreds of updates), so the decisions equal those of exact totals.
+constexpr float kNearZero = 0.5f;  // log2 units
+
+// P = L + c2v over a VN record (the fix-up / totals arithmetic), one lane
+__device__ __forceinline__ float exact_posterior(const ChunkState& s, const int4* __restrict__ rec, int vs4,
+                                                 int64_t lane) {
+  int4 t = __ldg(rec);
+  float acc = s.L[static_cast<int64_t>(t.x) * s.B + lane];
+  const int zero = s.zero_slot;
+  auto add = [&](int slot) {
+    if (slot != zero) acc += s.c2v[static_cast<int64_t>(slot) * s.B + lane];
+  };
+  add(t.y);
+  add(t.z);
+  add(t.w);
+  for (int r = 1; r < vs4 && t.w != zero; ++r) {
+    t = __ldg(rec + r);
+    add(t.x);
+    add(t.y);
+    add(t.z);
+    add(t.w);
+  }
+  return acc;
+}
+
+// Hard-decision sign words: sw[p][B/32], word 4W + i bit b = sign of lane
+// 4 (32 W + b) + i, one warp per (VN position, 128 lanes). B % 128 == 0.
+__global__ void __launch_bounds__(256) stream_signs(const int4* __restrict__ all_vn, int vs4, int n, ChunkState s) {
+  pdl_launch_next();
+  const int64_t QB = s.B / 4;
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  pdl_wait();
+  if (item >= n * QB) return;  // whole warps (n * QB is a multiple of 32)
+  const int p = static_cast<int>(item / QB);
+  const int64_t q = item - p * QB;
+  const States<4> st = load_states<4>(s, q);
+  const unsigned dn = done_bits<4>(st);
+  Vec<4> x;
+  if (dn != 0xfu) x = ldv<4>(s.P + static_cast<int64_t>(p) * s.B + 4 * q);
+  unsigned neg = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (dn & (1u << i)) continue;
+    float y = x.v[i];
+    if (fabsf(y) < kNearZero) y = exact_posterior(s, all_vn + static_cast<int64_t>(p) * vs4, vs4, 4 * q + i);
+    neg |= static_cast<unsigned>(y < 0.f) << i;  // tie -> 0 (decoder.hpp:166)
+  }
+  uint4 w;
+  w.x = __ballot_sync(0xffffffffu, neg & 1u);
+  w.y = __ballot_sync(0xffffffffu, neg & 2u);
+  w.z = __ballot_sync(0xffffffffu, neg & 4u);
+  w.w = __ballot_sync(0xffffffffu, neg & 8u);
+  if ((threadIdx.x & 31) == 0)
+    *reinterpret_cast<uint4*>(s.sw + static_cast<int64_t>(p) * (s.B / 32) + 4 * (q / 32)) = w;
+}
+
+// Syndrome weight per lane (decoder.hpp:129-137) from the sign words.
+template <int D, bool EXACT>
+__global__ void __launch_bounds__(256) stream_syndrome_sw(const int32_t* __restrict__ recs, int CS, int m,
+                                                          ChunkState s) {
+  pdl_launch_next();
+  const int64_t QB = s.B / 4;
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int r = static_cast<int>(item / QB);
+  const CnRecord<D, EXACT> cr(recs + static_cast<int64_t>(r < m ? r : 0) * CS, CS);
+  pdl_wait();
+  if (item == 0) s.ctl[0] = 0;  // the retire list of this iteration starts empty
+  if (item >= m * QB) return;
+  const int64_t q = item - r * QB;
+  if (done_bits<4>(s, q) == 0xfu) return;
+  const int b = static_cast<int>(q & 31);
+  const int64_t w0 = 4 * (q / 32);
+  unsigned par = 0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    if (!cr.has(k)) continue;
+    const uint4 w = *reinterpret_cast<const uint4*>(s.sw + static_cast<int64_t>(cr.var(k)) * (s.B / 32) + w0);
+    par ^= ((w.x >> b) & 1u) | ((w.y >> b) & 1u) << 1 | ((w.z >> b) & 1u) << 2 | ((w.w >> b) & 1u) << 3;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (par & (1u << i)) atomicAdd(s.weight + 4 * q + i, 1);
+}
+
+// Lanes [0, nb) hold frames [0, nb); the others idle.
+__global__ void stream_q_setup(ChunkState s, int64_t frames) {
+  const int64_t f = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (f < s.B) s.frame[f] = f < s.nb ? f : -1;
+  if (f == 0) {
+    *s.next = static_cast<unsigned long long>(s.nb);
+    s.ctl[0] = 0;
+    s.ctl[1] = s.nb;
+  }
+}
+
+// Per-lane bookkeeping after the syndrome test (decoder.hpp:166-177).
+__global__ void stream_q_iter_end(ChunkState s, int early_stop, int32_t* trace, int max_iters) {
+  pdl_enter();
+  const int64_t f = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (f >= s.B || (s.done[f] & 1)) return;
+  const int w = s.weight[f];
+  s.weight[f] = 0;
+  const int it = ++s.iters[f];
+  if (trace) trace[s.frame[f] * max_iters + it - 1] = w;
+  s.conv[f] = w == 0;
+  if ((w == 0 && early_stop) || it == max_iters) {
+    s.done[f] = kRetiring;
+    s.list[atomicAdd(s.ctl, 1)] = static_cast<int>(f);
+  } else {
+    s.done[f] = kLive;  // a fresh lane's first iteration is over
+  }
+}
+
+// Outputs of the retiring lanes (sim.hpp:119-123) and their refill with the
+// next frames; one block per retiring lane at a time.
+__global__ void __launch_bounds__(256) stream_q_retire(const DevGraph g, ChunkState s, const DecodeArgs a,
+                                                        const float* __restrict__ llr, int64_t frames) {
+  pdl_enter();
+  __shared__ int s_errs;
+  __shared__ long long s_new;
+  const int n = g.n, nbytes = (n + 7) / 8;
+  const int count = s.ctl[0];
+  unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
+  for (int e = blockIdx.x; e < count; e += gridDim.x) {
+    const int64_t f = s.list[e];
+    const int64_t fr = s.frame[f];
+    const int64_t w0 = 4 * (f / 128) + (f & 3);  // sign word of lane f, bit (f / 4) % 32
+    const int bit = static_cast<int>((f >> 2) & 31);
+    if (threadIdx.x == 0) s_errs = 0;
+    __syncthreads();
+    int errs = 0;
+    for (int b = threadIdx.x; b < nbytes; b += blockDim.x) {
+      unsigned byte = 0;
+      for (int j = 0; j < 8 && 8 * b + j < n; ++j) {
+        const int p = __ldg(g.vn_pos + 8 * b + j);
+        byte |= ((s.sw[static_cast<int64_t>(p) * (s.B / 32) + w0] >> bit) & 1u) << j;
+      }
+      if (a.bits) {
+        if (a.bits_packed) {
+          a.bits[fr * nbytes + b] = static_cast<uint8_t>(byte);
+        } else {
+          for (int j = 0; j < 8 && 8 * b + j < n; ++j) a.bits[fr * n + 8 * b + j] = static_cast<uint8_t>((byte >> j) & 1u);
+        }
+      }
+      errs += __popc(byte);
+    }
+    if (a.posterior)  // exact totals (decoder.hpp:162-165) of the stopped frame
+      for (int v = threadIdx.x; v < n; v += blockDim.x) {
+        const int p = __ldg(g.vn_pos + v);
+        a.posterior[fr * n + v] =
+            exact_posterior(s, reinterpret_cast<const int4*>(g.all_vn_rec) + static_cast<int64_t>(p) * g.vs4, g.vs4, f) *
+            kLn2;
+      }
+    if (errs) atomicAdd(&s_errs, errs);
+    __syncthreads();  // every read of this lane's state is done before the refill
+    if (threadIdx.x == 0) {
+      const int it = s.iters[f], cv = s.conv[f], be = s_errs;
+      if (a.iterations) a.iterations[fr] = it;
+      if (a.converged) a.converged[fr] = static_cast<uint8_t>(cv);
+      if (a.bit_errors) a.bit_errors[fr] = be;
+      c[0] += 1;
+      c[1] += be;
+      c[2] += be > 0;
+      c[3] += cv;
+      c[4] += it;
+      c[5] += cv ? it : 0;
+      const unsigned long long nf = atomicAdd(s.next, 1ull);
+      s_new = nf < static_cast<unsigned long long>(frames) ? static_cast<long long>(nf) : -1ll;
+      s.frame[f] = s_new;
+    }
+    __syncthreads();
+    const long long nf = s_new;
+    if (nf >= 0) {  // init_state (decoder.hpp:39-52) of the new frame: L only (fresh bits)
+      const float* row = llr + nf * n;
+      for (int v = threadIdx.x; v < n; v += blockDim.x)
+        s.L[static_cast<int64_t>(__ldg(g.vn_pos + v)) * s.B + f] = clamp_llr(__ldg(row + v)) * kLog2e;
+    }
+    if (threadIdx.x == 0) {
+      s.iters[f] = 0;
+      s.conv[f] = 0;
+      s.weight[f] = 0;
+      if (nf >= 0) {
+        s.done[f] = kFresh;
+      } else {
+        s.done[f] = kIdle;
+        atomicSub(s.ctl + 1, 1);
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && a.counters)
+    for (int i = 0; i < 6; ++i)
+      if (c[i]) atomicAdd(a.counters + i, c[i]);
+}
+
 struct StreamKernels {
-  void (*cn)(const int32_t*, int, int, ChunkState);
+  void (*cn)(const int32_t*, int, int, ChunkState, const uint32_t*);
   void (*syn)(const int32_t*, int, int, ChunkState);
-  void (*vnsum)(const int4*, int, int, ChunkState, int);
+  void (*vnsum)(const int4*, int, int, ChunkState, int, const uint32_t*);
+  void (*syn_sw)(const int32_t*, int, int, ChunkState);  // frame queue (V = 4)
 };
 
 template <int V>
 StreamKernels pick_v(const DevGraph& g) {
   switch (cn_bucket(g.max_cdeg, g.cregular)) {
-    case 3: return {stream_cn<3, true, V>, stream_syndrome<3, true, V>, stream_vnsum<V>};
-    case 6: return {stream_cn<6, true, V>, stream_syndrome<6, true, V>, stream_vnsum<V>};
-    case 8: return {stream_cn<8, false, V>, stream_syndrome<8, false, V>, stream_vnsum<V>};
-    case 16: return {stream_cn<16, false, V>, stream_syndrome<16, false, V>, stream_vnsum<V>};
-    default: return {nullptr, nullptr, nullptr};
+    case 3: return {stream_cn<3, true, V>, stream_syndrome<3, true, V>, stream_vnsum<V>, stream_syndrome_sw<3, true>};
+    case 6: return {stream_cn<6, true, V>, stream_syndrome<6, true, V>, stream_vnsum<V>, stream_syndrome_sw<6, true>};
+    case 8: return {stream_cn<8, false, V>, stream_syndrome<8, false, V>, stream_vnsum<V>, stream_syndrome_sw<8, false>};
+    case 16:
+      return {stream_cn<16, false, V>, stream_syndrome<16, false, V>, stream_vnsum<V>, stream_syndrome_sw<16, false>};
+    default: return {nullptr, nullptr, nullptr, nullptr};
   }
 }
 
@@ -485,14 +751,14 @@ int launch_stream_one(const DevGraph& g, const DecodeArgs& a, cudaStream_t st, c
         const int c0 = g.h_cn_off[grp], cn = g.h_cn_off[grp + 1] - c0;
         if (cn > 0) {
           err = launch_pdl(K.cn, blocks_for(cn * QB, tpb), tpb, st, pdl, g.cn_rec + static_cast<size_t>(c0) * g.cs,
-                           g.cs, cn, s);
+                           g.cs, cn, s, static_cast<const uint32_t*>(nullptr));
           ++launches;
         }
         const int x0 = g.h_fix_off[grp], xn = g.h_fix_off[grp + 1] - x0;
         if (xn > 0 && err == cudaSuccess) {
           err = launch_pdl(K.vnsum, blocks_for(xn * QB, tpb), tpb, st, pdl,
                            reinterpret_cast<const int4*>(g.fix_rec) + static_cast<size_t>(x0) * g.vs4, g.vs4, xn,
-                           s, 1);
+                           s, 1, static_cast<const uint32_t*>(nullptr));
           ++launches;
         }
         if (err != cudaSuccess) {
@@ -504,7 +770,8 @@ int launch_stream_one(const DevGraph& g, const DecodeArgs& a, cudaStream_t st, c
       const bool check = a.early_stop || a.trace || iter == a.max_iters;
       if (g.recompute && (check || !a.lazy_totals)) {
         err = launch_pdl(K.vnsum, blocks_for(g.n * QB, tpb), tpb, st, pdl,
-                         reinterpret_cast<const int4*>(g.all_vn_rec), g.vs4, g.n, s, 1);
+                         reinterpret_cast<const int4*>(g.all_vn_rec), g.vs4, g.n, s, 1,
+                         static_cast<const uint32_t*>(nullptr));
         ++launches;
       }
       if (!check || err != cudaSuccess) continue;
@@ -517,7 +784,7 @@ int launch_stream_one(const DevGraph& g, const DecodeArgs& a, cudaStream_t st, c
     if (dump) {
       if (g.recompute)
         K.vnsum<<<blocks_for(g.n * QB, tpb), tpb, 0, st>>>(reinterpret_cast<const int4*>(g.all_vn_rec), g.vs4, g.n,
-                                                           s, 0);
+                                                           s, 0, nullptr);
       stream_dump<<<blocks_for(static_cast<int64_t>(g.E) * s.nb, tpb), tpb, 0, st>>>(g, s, a.c2v_out, a.v2c_out,
                                                                                       f0);
       launches += 2;
@@ -535,6 +802,115 @@ int launch_stream_one(const DevGraph& g, const DecodeArgs& a, cudaStream_t st, c
   return static_cast<int>(err);
 }
 
+// LDPCB_STREAM_QUEUE=0 decodes early-stop batches chunk by chunk (every
+// chunk runs until its slowest frame stops; A/B and tests)
+bool stream_queue_enabled() {
+  const char* e = std::getenv("LDPCB_STREAM_QUEUE");
+  return !e || std::atoi(e) != 0;
+}
+
+// Early stop from a frame queue: B lanes (a multiple of 128) decode until
+// every frame of the batch has stopped. Per iteration: the groups' CN and
+// fix-up kernels, then sign words, syndrome weights, per-lane bookkeeping,
+// and retire + refill. The host reads the number of decoding lanes one
+// iteration behind, so the device never waits for the host.
+int launch_stream_queue(const DevGraph& g, const DecodeArgs& a, cudaStream_t st, int64_t B0) {
+  const StreamKernels K = pick_v<4>(g);
+  const int64_t B = (std::min<int64_t>(B0, a.frames) + 127) / 128 * 128;
+  ChunkState s;
+  s.B = B;
+  s.nb = static_cast<int>(std::min<int64_t>(B, a.frames));
+  s.zero_slot = g.n_slots - 1;
+  const size_t state = 4ull * (static_cast<size_t>(g.n_slots) + 2ull * g.n) * B;
+  const size_t lanes = 5 * 4 * B + 8 * B + 4 * B + 64;
+  const size_t signs = 4ull * g.n * (B / 32);
+  char* mem = nullptr;
+  cudaError_t err = cudaMallocAsync(reinterpret_cast<void**>(&mem), state + lanes + signs, st);
+  if (err != cudaSuccess) return static_cast<int>(err);
+  s.c2v = reinterpret_cast<float*>(mem);
+  s.P = s.c2v + static_cast<size_t>(g.n_slots) * B;
+  s.L = s.P + static_cast<size_t>(g.n) * B;
+  s.done = reinterpret_cast<int*>(s.L + static_cast<size_t>(g.n) * B);
+  s.weight = s.done + B;
+  s.iters = s.weight + B;
+  s.conv = s.iters + B;
+  s.berr = s.conv + B;
+  s.frame = reinterpret_cast<int64_t*>(s.berr + B);
+  s.list = reinterpret_cast<int*>(s.frame + B);
+  s.ctl = s.list + B;
+  s.next = reinterpret_cast<unsigned long long*>(s.ctl + 8);
+  s.sw = reinterpret_cast<unsigned*>(mem + state + lanes);
+  // the host's view of the decoding-lane count, one slot per parity of the iteration
+  thread_local int* host_live = nullptr;
+  if (!host_live && cudaMallocHost(reinterpret_cast<void**>(&host_live), 2 * sizeof(int)) != cudaSuccess) {
+    host_live = nullptr;
+    cudaFreeAsync(mem, st);
+    return static_cast<int>(cudaErrorMemoryAllocation);
+  }
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  for (auto& e : ev)
+    if (err == cudaSuccess) err = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  const int tpb = 256;
+  const int64_t QB = B / 4;
+  const bool pdl = stream_pdl();
+  int launches = 0;
+  int sms = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if (err == cudaSuccess) err = cudaMemsetAsync(s.c2v, 0, 4ull * g.n_slots * B, st);
+  if (err == cudaSuccess && a.trace) err = cudaMemsetAsync(a.trace, 0xff, 4ull * a.frames * a.max_iters, st);
+  if (err == cudaSuccess) {
+    stream_init<<<dim3((g.n + 31) / 32, static_cast<unsigned>((B + 31) / 32)), dim3(32, 8), 0, st>>>(g.n, g.vn_pos,
+                                                                                                     a.llr, s);
+    stream_q_setup<<<blocks_for(B, tpb), tpb, 0, st>>>(s, a.frames);
+    launches += 2;
+    err = cudaGetLastError();
+  }
+  const auto* fix4 = reinterpret_cast<const int4*>(g.fix_rec);
+  for (int64_t it = 0; err == cudaSuccess; ++it) {
+    for (int grp = 0; grp < g.G && err == cudaSuccess; ++grp) {
+      const int c0 = g.h_cn_off[grp], cn = g.h_cn_off[grp + 1] - c0;
+      if (cn > 0) {
+        err = launch_pdl(K.cn, blocks_for(cn * QB, tpb), tpb, st, pdl, g.cn_rec + static_cast<size_t>(c0) * g.cs, g.cs,
+                         cn, s, g.cn_fresh + c0);
+        ++launches;
+      }
+      const int x0 = g.h_fix_off[grp], xn = g.h_fix_off[grp + 1] - x0;
+      if (xn > 0 && err == cudaSuccess) {
+        err = launch_pdl(K.vnsum, blocks_for(xn * QB, tpb), tpb, st, pdl, fix4 + static_cast<size_t>(x0) * g.vs4,
+                         g.vs4, xn, s, 1, g.fix_fresh + x0);
+        ++launches;
+      }
+    }
+    if (err != cudaSuccess) break;
+    err = launch_pdl(stream_signs, blocks_for(g.n * QB, tpb), tpb, st, pdl,
+                     reinterpret_cast<const int4*>(g.all_vn_rec), g.vs4, g.n, s);
+    if (err == cudaSuccess)
+      err = launch_pdl(K.syn_sw, blocks_for(g.m * QB, tpb), tpb, st, pdl, g.all_rec, g.cs, g.m, s);
+    if (err == cudaSuccess)
+      err = launch_pdl(stream_q_iter_end, blocks_for(B, tpb), tpb, st, pdl, s, a.early_stop, a.trace, a.max_iters);
+    if (err == cudaSuccess)
+      err = launch_pdl(stream_q_retire, static_cast<unsigned>(4 * sms), tpb, st, pdl, g, s, a, a.llr, a.frames);
+    launches += 4;
+    const int k = static_cast<int>(it & 1);
+    if (err == cudaSuccess) err = cudaMemcpyAsync(host_live + k, s.ctl + 1, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (err == cudaSuccess) err = cudaEventRecord(ev[k], st);
+    if (err != cudaSuccess || it == 0) continue;
+    // the previous iteration's count: zero means this iteration found every
+    // lane idle (its kernels exit at once) and the batch is done
+    err = cudaEventSynchronize(ev[k ^ 1]);
+    if (err == cudaSuccess && host_live[k ^ 1] == 0) break;
+  }
+  note_launches(launches);
+  for (auto e : ev)
+    if (e) cudaEventDestroy(e);
+  cudaFreeAsync(mem, st);
+  return static_cast<int>(err);
+}
+
 }  // namespace
 
 int launch_stream(const DevGraph& g, const DecodeArgs& a, void* stream_v, Plan* used) {
@@ -542,6 +918,11 @@ int launch_stream(const DevGraph& g, const DecodeArgs& a, void* stream_v, Plan* 
   if (used) *used = p;
   if (p.kernel == 0) return static_cast<int>(cudaErrorInvalidConfiguration);
   if (a.frames <= 0) return 0;
+  // early stop: frames stream through the lanes (frame queue) when the tables
+  // allow it (every CN grouped, every VN touched, stride-4 lanes)
+  if (a.early_stop && a.max_subiters == 0 && g.covers && g.cn_fresh && g.fix_fresh && stream_lanes() == 4 &&
+      stream_queue_enabled())
+    return launch_stream_queue(g, a, static_cast<cudaStream_t>(stream_v), p.fpc);
   return launch_stream_one(g, a, static_cast<cudaStream_t>(stream_v), p);
 }
 
