@@ -15,6 +15,7 @@ constexpr float kLn2 = 0.69314718055994531f;
 constexpr float kClampB = 43.280851226668897f;  // 30 * log2(e)
 
 
+#ifndef LDPCB_EXP_NOMUFU
 __device__ __forceinline__ float mufu_ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -25,6 +26,10 @@ __device__ __forceinline__ float mufu_lg2(float x) {
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+#else  // timing experiment only (scripts/exp_builds.sh): wrong results
+__device__ __forceinline__ float mufu_ex2(float x) { return fmaf(x, 0.01f, 1.0f); }
+__device__ __forceinline__ float mufu_lg2(float x) { return fmaf(x, 0.5f, -0.5f); }
+#endif
 
 __device__ __forceinline__ float clamp_llr(float x) { return fminf(fmaxf(x, -kClamp), kClamp); }
 __device__ __forceinline__ float clamp_bits(float x) { return fminf(fmaxf(x, -kClampB), kClampB); }

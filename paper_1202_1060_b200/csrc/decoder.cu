@@ -566,12 +566,18 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
             cn_update<D, EXACT, FPC, FV, false>(c2v, P, Rec(rec + j * CS, CS), live);
         }
       }
+#ifndef LDPCB_EXP_NOSYNC1
       __syncthreads();
+#endif
       PT_MARK(pt_b);
       pin(fix_first);
       // VNs shared by two or more CNs of the group: exact re-sum (a stopped
       // frame re-sums to the value it already holds)
+#ifdef LDPCB_EXP_NOFIX  // timing experiment only: wrong results
+      if (false) {
+#else
       if (xn > 0) {
+#endif
         if (live && j0 < xn) {
           if (vs16) {
             const int4* rec = fix16 + static_cast<size_t>(x0) * vs16;

@@ -419,10 +419,11 @@ __global__ void stream_dump(const DevGraph g, ChunkState s, float* c2v_out, floa
 // posteriors are masked by the fresh bits during its first iteration.
 // Posteriors are kept in place between syndrome tests (no all-VN re-sum per
 // iteration): the hard decision of a posterior within kNearZero of 0 is taken
-// from its exact re-sum (P = L + sum c2v, decoder.hpp:162-166), far outside
-// the rounding the in-place updates can accumulate (< 1e-2 in log2 units over
-// hundreds of updates), so the decisions equal those of exact totals.
-constexpr float kNearZero = 0.5f;  // log2 units
+// from its exact re-sum (P = L + sum c2v, decoder.hpp:162-166). An in-place
+// update P += c_new - c_old rounds at most ulp(43 * 2) = 7.6e-6 (messages are
+// clamped to 43.3 in log2 units), so 60 updates (30 iterations, two touches
+// each) stay below 5e-4: decisions outside kNearZero equal those of exact totals.
+constexpr float kNearZero = 2e-3f;  // log2 units
 
 // P = L + c2v over a VN record (the fix-up / totals arithmetic), one lane
 __device__ __forceinline__ float exact_posterior(const ChunkState& s, const int4* __restrict__ rec, int vs4,
@@ -461,13 +462,37 @@ __global__ void __launch_bounds__(256) stream_signs(const int4* __restrict__ all
   Vec<4> x;
   if (dn != 0xfu) x = ldv<4>(s.P + static_cast<int64_t>(p) * s.B + 4 * q);
   unsigned neg = 0;
+  bool near = false;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    if (dn & (1u << i)) continue;
-    float y = x.v[i];
-    if (fabsf(y) < kNearZero) y = exact_posterior(s, all_vn + static_cast<int64_t>(p) * vs4, vs4, 4 * q + i);
-    neg |= static_cast<unsigned>(y < 0.f) << i;  // tie -> 0 (decoder.hpp:166)
+  for (int i = 0; i < 4; ++i) near |= !(dn & (1u << i)) && fabsf(x.v[i]) < kNearZero;
+  if (near) {  // rare: the exact totals of the quad (16-byte loads, as stream_vnsum)
+    const int4* rec = all_vn + static_cast<int64_t>(p) * vs4;
+    int4 t = __ldg(rec);
+    Vec<4> acc = ldv<4>(s.L + static_cast<int64_t>(t.x) * s.B + 4 * q);
+    const int zero = s.zero_slot;
+    auto add = [&](int slot) {
+      if (slot == zero) return;
+      const Vec<4> c = ldv<4>(s.c2v + static_cast<int64_t>(slot) * s.B + 4 * q);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc.v[i] += c.v[i];
+    };
+    add(t.y);
+    add(t.z);
+    add(t.w);
+    for (int r = 1; r < vs4 && t.w != zero; ++r) {
+      t = __ldg(rec + r);
+      add(t.x);
+      add(t.y);
+      add(t.z);
+      add(t.w);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (fabsf(x.v[i]) < kNearZero) x.v[i] = acc.v[i];
   }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (!(dn & (1u << i))) neg |= static_cast<unsigned>(x.v[i] < 0.f) << i;  // tie -> 0 (decoder.hpp:166)
   uint4 w;
   w.x = __ballot_sync(0xffffffffu, neg & 1u);
   w.y = __ballot_sync(0xffffffffu, neg & 2u);
