@@ -67,6 +67,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=30.0, help="CPU sample duration per workload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--kernel", type=int, default=0,
+                    help="0 library plan, 1 posterior-based resident, 2 HBM-streamed, 3 posterior-free resident (A/B)")
     ap.add_argument("--fpc", type=int, default=0, help="frames per CTA (0 = library plan)")
     ap.add_argument("--threads", type=int, default=0, help="threads per CTA (0 = library plan)")
     return ap.parse_args()
@@ -258,6 +260,7 @@ def measure_leg(args, name, world, rank, local):
         ebn0 = 1.1
     sigma2 = P.sigma2_from_ebn0(ebn0, g.rate)
     P.set_tuning(args.fpc, args.threads)
+    P.set_kernel(args.kernel if name == "c5_n1008" else 0)
     B = args.frames or DEFAULT_FRAMES[name]
     n = g.n_vars
     K = n - g.n_checks
@@ -338,7 +341,7 @@ def measure_leg(args, name, world, rank, local):
         peak = n_sm * MUFU_PER_SM_CLK * sm_max * 1e6
         roofline = {"bound": "sfu", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "GMUFU/s",
                     "frac": achieved / peak, "traffic": traffic,
-                    "note": f"decode_resident: {MUFU_PER_EDGE} MUFU per CN-edge update x {s.edge_updates_per_iter} "
+                    "note": f"{'decode_direct' if pl['kernel'] >= 20 else 'decode_resident'}: {MUFU_PER_EDGE} MUFU per CN-edge update x {s.edge_updates_per_iter} "
                             f"edge updates/iter x {args.iters} iters x {B} frames per launch / CUDA-event launch "
                             f"time {kernel_ms:.3f} ms; peak = {n_sm} SMs x {MUFU_PER_SM_CLK}/clk x {sm_max:.0f} MHz "
                             "(MEASURED_PEAKS sm_max_mhz)"}

@@ -195,15 +195,18 @@ int ldpcb_run_subiterations_device(ldpcb_code code, ldpcb_schedule s, int64_t fr
 /* ---- introspection / tuning --------------------------------------------- */
 
 /* kernel: 2 = HBM-streamed (fpc = frames per chunk); SMEM-resident plans
- * report 10 + frames_per_thread (11, 12) with fpc = frames per CTA */
+ * report 10 + frames_per_thread (11, 12) with fpc = frames per CTA; the
+ * posterior-free resident kernel reports 20 + frame pairs per CTA (21..23) */
 int ldpcb_decode_plan(ldpcb_code code, ldpcb_schedule s, int64_t frames, int32_t *kernel, int32_t *fpc,
                       int32_t *threads, int32_t *smem_bytes, int32_t *degree_bucket);
 /* 0 = automatic */
 int ldpcb_set_tuning(int frames_per_cta, int threads);
 /* frames per thread of the resident kernel: 0 = automatic, 1 or 2 */
 int ldpcb_set_frames_per_thread(int fv);
-/* 0 = automatic (resident when a frame fits shared memory), 1 = resident
- * only, 2 = HBM-streamed */
+/* 0 = automatic (resident when a frame fits shared memory; the posterior-free
+ * resident kernel where the code and schedule qualify), 1 = resident
+ * posterior-based kernel only, 2 = HBM-streamed, 3 = posterior-free resident
+ * kernel (decodes fail when the code or the schedule does not qualify) */
 int ldpcb_set_kernel(int kernel);
 /* 1 (default): in iterations that do not test the syndrome, skip the exact
  * re-summation of the posteriors (in-place updates carry them); the totals

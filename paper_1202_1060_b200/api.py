@@ -637,7 +637,8 @@ def set_tuning(frames_per_cta: int = 0, threads: int = 0, frames_per_thread: int
 
 
 def set_kernel(kernel: int = 0) -> None:
-    """0 automatic, 1 shared-memory resident only, 2 HBM-streamed."""
+    """0 automatic, 1 shared-memory resident (posterior-based kernel) only,
+    2 HBM-streamed, 3 posterior-free resident kernel (direct.cu)."""
     check(lib.ldpcb_set_kernel(kernel))
 
 

@@ -1330,6 +1330,14 @@ int launch_gen_groups(const DevGraph& g, int64_t frame0, int64_t frames, int lis
 
 Plan plan_decode(const DevGraph& g, int64_t frames, bool early_stop) {
   if (g.per_frame) return plan_resident(g, frames, early_stop);  // per-frame groups: resident kernel only
+  // the posterior-free kernel (direct.cu) wherever its tables exist and no
+  // explicit resident tuning was requested; kernel 3 forces it
+  const int force = g_force_kernel.load();
+  if (force == 3 ||
+      (force == 0 && g.d_ng > 0 && g_tune_fpc.load() == 0 && g_tune_threads.load() == 0 && g_tune_fv.load() == 0)) {
+    const Plan d = plan_direct(g, frames);
+    if (d.kernel == 3 || force == 3) return d;
+  }
   if (g_force_kernel.load() == 2) return plan_stream(g, frames);
   Plan p = plan_resident(g, frames, early_stop);
   if (p.kernel == 0 && g_force_kernel.load() != 1) p = plan_stream(g, frames);
@@ -1431,6 +1439,7 @@ int launch_decode(const DevGraph& g, const DecodeArgs& a_in, void* stream, Plan*
   a.lazy_totals = g_lazy_totals.load();
   const Plan p = plan_decode(g, a.frames, a.early_stop != 0);
   if (p.kernel == 2) return launch_stream(g, a, stream, used);
+  if (p.kernel == 3) return launch_direct(g, a, stream, used);
   if (used) *used = p;
   if (p.kernel == 0) return static_cast<int>(cudaErrorInvalidConfiguration);
   if (a.frames <= 0) return 0;

@@ -145,6 +145,31 @@ struct KernelTables {
 // cs = CN record stride in ints (>= 2 + max CN degree, multiple of 4)
 KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, bool regular_rows);
 
+
+// Tables of the direct (posterior-free) resident kernel (direct.cu) for codes
+// whose VNs have degree <= 3 and whose CNs all have degree 6. A frame pair's
+// state is one array of 8-byte cells (two frames per cell): a c2v cell per
+// edge, an L cell per VN (clamped channel LLR) and one constant-zero cell.
+// A CN item forms v2c_k = L_v + c2v_a + c2v_b from the OTHER two edges of
+// each of its VNs (a < b in CN order; zero cell past the VN's degree), so no
+// posterior array, no in-place update and no fix-up pass exist. Every field is
+// a 16-bit byte offset into the pair's cell array (cells * 8 <= 65536):
+//   CN record  12 ints: word 2k = own_k | L_k << 16, word 2k+1 = a_k | b_k << 16
+//   VN record   2 ints, indexed by VN position: c_0 | c_1 << 16, c_2 (hard decisions)
+//   all_cn      4 ints per CN: the six VN positions as 16-bit fields (syndrome)
+//   edge_rec    2 ints per CN-major edge id, same fields as a CN record (state dumps)
+// Cell ids are bank-coloured (host_direct.cpp): the cells a half-warp touches
+// in one instruction fall in distinct banks where possible.
+struct DirectTables {
+  bool ok = false;
+  int ng = 1;        // frame pairs per CTA the colouring assumed
+  int cells = 0;     // cells per frame pair, multiple of 16; the last one is the zero cell
+  int l_base = 0;    // L cell of position p = l_base + p
+  int max_items = 0;
+  std::vector<int32_t> cn_off, cn_rec, vn_rec, all_cn, edge_rec, vn_pos;
+};
+DirectTables direct_tables(const CodeData& c, const ScheduleData& s, int ng);
+
 ScheduleData schedule_from_groups(const CodeData& c, Kind kind, const Rows& groups);
 ScheduleData flooding_schedule(const CodeData& c);
 ScheduleData reference_random_schedule(const CodeData& c, Kind kind, int G, double overlap, uint64_t seed);

@@ -33,6 +33,14 @@ struct DevGraph {
   const uint32_t* cn_fresh = nullptr;   // per cn_rec record
   const uint32_t* fix_fresh = nullptr;  // per fix_rec record
   bool covers = false;
+  // direct (posterior-free) kernel tables (host.hpp DirectTables); d_ng = 0: none
+  int d_ng = 0, d_cells = 0, d_l_base = 0, d_max_items = 0;
+  const int32_t* d_cn_off = nullptr;
+  const int32_t* d_cn_rec = nullptr;
+  const int32_t* d_vn_rec = nullptr;
+  const int32_t* d_all_cn = nullptr;
+  const int32_t* d_edge_rec = nullptr;
+  const int32_t* d_vn_pos = nullptr;
   // per-frame random grouping (host.hpp ScheduleData::per_frame)
   bool per_frame = false, regroup = false, balanced = false;
   int nominal = 0, k_overlap = 0, list_slots = 0;
@@ -76,7 +84,7 @@ inline int cn_bucket(int max_cdeg, bool cregular) {
 inline int cn_record_stride(int bucket) { return (2 + bucket + 3) / 4 * 4; }
 
 struct Plan {
-  int kernel = 0;  // 1 = SMEM-resident frame-interleaved, 2 = HBM-streamed
+  int kernel = 0;  // 1 = SMEM-resident frame-interleaved, 2 = HBM-streamed, 3 = SMEM-resident direct (direct.cu)
   int fpc = 0;     // frames per CTA
   int fv = 1;      // frames per thread (resident kernel)
   int threads = 0;
@@ -99,7 +107,11 @@ int launch_check_update(int degree, int64_t rows, const float* v2c, float* c2v, 
 
 void set_tuning(int fpc, int threads);
 void set_frames_per_thread(int fv);
-void set_force_kernel(int kernel);  // 0 auto, 1 resident, 2 streamed
+void set_force_kernel(int kernel);  // 0 auto, 1 resident (posterior-based), 2 streamed, 3 direct
+// posterior-free resident kernel (direct.cu): (3,6)-type codes, groups of at most one CN item per thread
+Plan plan_direct(const DevGraph& g, int64_t frames);
+int launch_direct(const DevGraph& g, const DecodeArgs& a, void* stream, Plan* used);
+bool direct_enabled();
 void note_launches(int n);
 // HBM-streamed decoder (stream.cu): frames whose state does not fit one SM
 int launch_stream(const DevGraph& g, const DecodeArgs& a, void* stream, Plan* used);

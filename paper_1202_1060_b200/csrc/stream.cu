@@ -168,7 +168,9 @@ __global__ void stream_init(int n, const int32_t* __restrict__ pos, const float*
 // queue only, else null): per-record bits of KernelTables::cn_fresh for lanes
 // in the first iteration of a refilled frame (old c2v = 0, P = L at a VN's
 // first touch), which is what a zeroed c2v and P = L would give.
-template <int D, bool EXACT, int V>
+// FRESH = false compiles none of the fresh-frame code (the fixed-iteration
+// and chunked early-stop paths: 106 registers, two CTAs per SM; with it 147).
+template <int D, bool EXACT, int V, bool FRESH>
 __global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ recs, int CS, int count, ChunkState s,
                                                  const uint32_t* __restrict__ fresh) {
   pdl_launch_next();
@@ -184,8 +186,12 @@ __global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ rec
   const States<V> st = load_states<V>(s, q);
   const unsigned dn = done_bits<V>(st);
   if (dn == (1u << V) - 1) return;
-  const unsigned fr = fresh ? fresh_bits<V>(st) : 0u;
-  const uint32_t fbits = fr ? __ldg(fresh + j) : 0u;
+  unsigned fr = 0u;
+  uint32_t fbits = 0u;
+  if constexpr (FRESH) {
+    fr = fresh_bits<V>(st);
+    fbits = fr ? __ldg(fresh + j) : 0u;
+  }
   const int base = cr.slot();
   const unsigned mask = cr.mask();
   const int deg = cr.deg();
@@ -195,7 +201,7 @@ __global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ rec
     if (cr.has(k)) {
       pv[k] = ldv<V>(s.P + static_cast<int64_t>(cr.var(k)) * s.B + V * q);
       old[k] = ldv<V>(s.c2v + static_cast<int64_t>(base + k) * s.B + V * q);
-      if (fr && (fbits & (1u << k))) {  // first touch of this VN in a fresh frame: P = L
+      if (FRESH && fr && (fbits & (1u << k))) {  // first touch of this VN in a fresh frame: P = L
         const Vec<V> l = ldv<V>(s.L + static_cast<int64_t>(cr.var(k)) * s.B + V * q);
 #pragma unroll
         for (int i = 0; i < V; ++i)
@@ -209,11 +215,31 @@ __global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ rec
   Vec<V> out[D];
 #pragma unroll
   for (int i = 0; i < V; ++i) {
-    const bool zero_old = (fr & (1u << i)) && (fbits >> 31);  // first processing of this CN
+    const bool zero_old = FRESH && (fr & (1u << i)) && (fbits >> 31);  // first processing of this CN
     float x[D];
 #pragma unroll
     for (int k = 0; k < D; ++k) x[k] = pv[k].v[i] - (zero_old ? 0.f : old[k].v[i]);
     boxplus_row<D, EXACT>(x, deg, [&](int k, float c) { out[k].v[i] = c; });
+  }
+  if constexpr (!FRESH) {
+    // frames that already stopped (decoder.hpp:173-177) keep their state
+#pragma unroll
+    for (int i = 0; i < V; ++i)
+      if (dn & (1u << i))
+#pragma unroll
+        for (int k = 0; k < D; ++k) out[k].v[i] = old[k].v[i];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      if (!cr.has(k)) continue;
+      stv<V>(s.c2v + static_cast<int64_t>(base + k) * s.B + V * q, out[k]);
+      if (mask & (1u << k)) {
+        Vec<V> p;
+#pragma unroll
+        for (int i = 0; i < V; ++i) p.v[i] = (pv[k].v[i] - old[k].v[i]) + out[k].v[i];
+        stv<V>(s.P + static_cast<int64_t>(cr.var(k)) * s.B + V * q, p);
+      }
+    }
+    return;
   }
 #pragma unroll
   for (int k = 0; k < D; ++k) {
@@ -236,7 +262,7 @@ __global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ rec
 // of decoder.hpp:162-165), over (VN record, V-frame vector) items.
 // Records are padded with the zero slot after the VN's last edge; the loop
 // stops there (a warp serves one VN, so the exit is warp-uniform).
-template <int V>
+template <int V, bool FRESH>
 __global__ void __launch_bounds__(256) stream_vnsum(const int4* __restrict__ recs, int vs4, int count, ChunkState s,
                                                     int skip_done, const uint32_t* __restrict__ fresh) {
   pdl_launch_next();
@@ -252,14 +278,18 @@ __global__ void __launch_bounds__(256) stream_vnsum(const int4* __restrict__ rec
   if (skip_done && done_bits<V>(st) == (1u << V) - 1) return;
   // fresh lanes (frame queue): slot fields of CNs not processed yet in the
   // frame's first iteration hold the previous frame's c2v and count as 0
-  const unsigned fr = fresh ? fresh_bits<V>(st) : 0u;
-  const uint32_t valid = fr ? __ldg(fresh + j) : ~0u;
+  unsigned fr = 0u;
+  uint32_t valid = ~0u;
+  if constexpr (FRESH) {
+    fr = fresh_bits<V>(st);
+    valid = fr ? __ldg(fresh + j) : ~0u;
+  }
   const int v = t.x;
   Vec<V> acc = ldv<V>(s.L + static_cast<int64_t>(v) * s.B + V * q);
   int field = 0;
   auto add = [&](int slot) {
     const Vec<V> c = ldv<V>(s.c2v + static_cast<int64_t>(slot) * s.B + V * q);
-    const bool stale = !((valid >> field) & 1u);
+    const bool stale = FRESH && !((valid >> field) & 1u);
 #pragma unroll
     for (int i = 0; i < V; ++i) acc.v[i] += (stale && (fr & (1u << i))) ? 0.f : c.v[i];
   };
@@ -646,17 +676,25 @@ struct StreamKernels {
   void (*syn)(const int32_t*, int, int, ChunkState);
   void (*vnsum)(const int4*, int, int, ChunkState, int, const uint32_t*);
   void (*syn_sw)(const int32_t*, int, int, ChunkState);  // frame queue (V = 4)
+  // frame queue: the same kernels with the fresh-frame code compiled in
+  void (*cn_fresh)(const int32_t*, int, int, ChunkState, const uint32_t*);
+  void (*vnsum_fresh)(const int4*, int, int, ChunkState, int, const uint32_t*);
 };
+
+template <int D, bool EXACT, int V>
+StreamKernels pick_dv() {
+  return {stream_cn<D, EXACT, V, false>, stream_syndrome<D, EXACT, V>,       stream_vnsum<V, false>,
+          stream_syndrome_sw<D, EXACT>,  stream_cn<D, EXACT, V, true>,       stream_vnsum<V, true>};
+}
 
 template <int V>
 StreamKernels pick_v(const DevGraph& g) {
   switch (cn_bucket(g.max_cdeg, g.cregular)) {
-    case 3: return {stream_cn<3, true, V>, stream_syndrome<3, true, V>, stream_vnsum<V>, stream_syndrome_sw<3, true>};
-    case 6: return {stream_cn<6, true, V>, stream_syndrome<6, true, V>, stream_vnsum<V>, stream_syndrome_sw<6, true>};
-    case 8: return {stream_cn<8, false, V>, stream_syndrome<8, false, V>, stream_vnsum<V>, stream_syndrome_sw<8, false>};
-    case 16:
-      return {stream_cn<16, false, V>, stream_syndrome<16, false, V>, stream_vnsum<V>, stream_syndrome_sw<16, false>};
-    default: return {nullptr, nullptr, nullptr, nullptr};
+    case 3: return pick_dv<3, true, V>();
+    case 6: return pick_dv<6, true, V>();
+    case 8: return pick_dv<8, false, V>();
+    case 16: return pick_dv<16, false, V>();
+    default: return {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   }
 }
 
@@ -899,14 +937,14 @@ int launch_stream_queue(const DevGraph& g, const DecodeArgs& a, cudaStream_t st,
     for (int grp = 0; grp < g.G && err == cudaSuccess; ++grp) {
       const int c0 = g.h_cn_off[grp], cn = g.h_cn_off[grp + 1] - c0;
       if (cn > 0) {
-        err = launch_pdl(K.cn, blocks_for(cn * QB, tpb), tpb, st, pdl, g.cn_rec + static_cast<size_t>(c0) * g.cs, g.cs,
-                         cn, s, g.cn_fresh + c0);
+        err = launch_pdl(K.cn_fresh, blocks_for(cn * QB, tpb), tpb, st, pdl,
+                         g.cn_rec + static_cast<size_t>(c0) * g.cs, g.cs, cn, s, g.cn_fresh + c0);
         ++launches;
       }
       const int x0 = g.h_fix_off[grp], xn = g.h_fix_off[grp + 1] - x0;
       if (xn > 0 && err == cudaSuccess) {
-        err = launch_pdl(K.vnsum, blocks_for(xn * QB, tpb), tpb, st, pdl, fix4 + static_cast<size_t>(x0) * g.vs4,
-                         g.vs4, xn, s, 1, g.fix_fresh + x0);
+        err = launch_pdl(K.vnsum_fresh, blocks_for(xn * QB, tpb), tpb, st, pdl,
+                         fix4 + static_cast<size_t>(x0) * g.vs4, g.vs4, xn, s, 1, g.fix_fresh + x0);
         ++launches;
       }
     }

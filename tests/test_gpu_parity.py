@@ -249,7 +249,7 @@ def test_counters_agree_with_outputs(P, torch, orc):
     assert cnt.cpu().tolist() == [int(x) for x in want]
 
 
-@pytest.mark.parametrize("fpc,threads", [(1, 96), (2, 0), (4, 512), (8, 0), (8, 256)])
+@pytest.mark.parametrize("fpc,threads", [(1, 96), (2, 0), (4, 256), (8, 0), (8, 256)])
 def test_tuning_and_ragged_batches_are_identical(P, torch, orc, fpc, threads):
     g = P.configs.c1_code()
     s = P.configs.c1_schedules(g)["ndgsbp"]
