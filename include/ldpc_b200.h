@@ -196,7 +196,7 @@ int ldpcb_run_subiterations_device(ldpcb_code code, ldpcb_schedule s, int64_t fr
 
 /* kernel: 2 = HBM-streamed (fpc = frames per chunk); SMEM-resident plans
  * report 10 + frames_per_thread (11, 12) with fpc = frames per CTA; the
- * posterior-free resident kernel reports 20 + frame pairs per CTA (21..23) */
+ * posterior-free resident kernel reports 20 + frames per thread (22, 24) */
 int ldpcb_decode_plan(ldpcb_code code, ldpcb_schedule s, int64_t frames, int32_t *kernel, int32_t *fpc,
                       int32_t *threads, int32_t *smem_bytes, int32_t *degree_bucket);
 /* 0 = automatic */

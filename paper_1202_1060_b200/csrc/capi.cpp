@@ -114,8 +114,8 @@ struct SchedImpl {
   struct Dev {
     int32_t *cn_off, *cn_rec, *fix_off, *fix_rec, *fix_rec16, *tot_rec16, *all_vn_rec, *tot_vn_rec, *all_rec, *edge_slot, *vn_pos;
     uint32_t *cn_fresh, *fix_fresh;
-    int32_t *d_cn_off = nullptr, *d_cn_rec = nullptr, *d_vn_rec = nullptr, *d_all_cn = nullptr, *d_edge_rec = nullptr,
-            *d_vn_pos = nullptr;
+    int32_t *d_cn_rec = nullptr, *d_vn_rec = nullptr, *d_all_cn = nullptr, *d_edge_rec = nullptr,
+            *d_vn_pos = nullptr, *d_vn_hold = nullptr;
     std::vector<void*> ptrs;
   };
   std::map<int, Dev> dev;
@@ -146,13 +146,14 @@ struct SchedImpl {
     x.ptrs = {x.cn_off,     x.cn_rec,     x.fix_off, x.fix_rec,   x.fix_rec16, x.tot_rec16,
               x.all_vn_rec, x.tot_vn_rec, x.all_rec, x.edge_slot, x.vn_pos,  x.cn_fresh, x.fix_fresh};
     if (direct.ok) {
-      x.d_cn_off = upload(direct.cn_off);
       x.d_cn_rec = upload(direct.cn_rec);
       x.d_vn_rec = upload(direct.vn_rec);
       x.d_all_cn = upload(direct.all_cn);
       x.d_edge_rec = upload(direct.edge_rec);
       x.d_vn_pos = upload(direct.vn_pos);
-      for (void* q : {static_cast<void*>(x.d_cn_off), static_cast<void*>(x.d_cn_rec), static_cast<void*>(x.d_vn_rec),
+      x.d_vn_hold = upload(direct.vn_hold);
+      x.ptrs.push_back(x.d_vn_hold);
+      for (void* q : {static_cast<void*>(x.d_cn_rec), static_cast<void*>(x.d_vn_rec),
                       static_cast<void*>(x.d_all_cn), static_cast<void*>(x.d_edge_rec), static_cast<void*>(x.d_vn_pos)})
         x.ptrs.push_back(q);
     }
@@ -199,10 +200,10 @@ int make_sched(const std::shared_ptr<CodeImpl>& code, ldpcb::ScheduleData s, ldp
     const bool packed = (bucket == 3 || bucket == 6) && h.n < 65536 && static_cast<long long>(h.m) * 7 + 1 < (1 << 24);
     impl->tables = ldpcb::kernel_tables(h, impl->host, packed ? 4 : ldpcb::cn_record_stride(bucket), code->cregular);
     // the posterior-free kernel's tables (direct.cu) where the code and the groups qualify;
-    // LDPCB_DIRECT_NG = frame pairs per CTA its bank colouring assumes (1..3)
+    // LDPCB_DIRECT_FV = frames per thread (2 or 4; A/B)
     if (ldpcb::direct_enabled()) {
-      const char* e = std::getenv("LDPCB_DIRECT_NG");
-      impl->direct = ldpcb::direct_tables(h, impl->host, e ? std::atoi(e) : 1);
+      const char* e = std::getenv("LDPCB_DIRECT_FV");
+      impl->direct = ldpcb::direct_tables(h, impl->host, e ? std::atoi(e) : 2);
     }
   }
   *out = new ldpcb_schedule_s{impl};
@@ -301,16 +302,17 @@ ldpcb::DevGraph dev_graph(ldpcb_code code, ldpcb_schedule s) {
   g.covers = t.covers;
   const auto& dt = s->impl->direct;
   if (dt.ok) {
-    g.d_ng = dt.ng;
+    g.d_fv = dt.fv;
     g.d_cells = dt.cells;
     g.d_l_base = dt.l_base;
     g.d_max_items = dt.max_items;
-    g.d_cn_off = d.d_cn_off;
+    for (size_t i = 0; i < dt.cn_off.size(); ++i) g.d_goff[i] = static_cast<uint16_t>(dt.cn_off[i]);
     g.d_cn_rec = d.d_cn_rec;
     g.d_vn_rec = d.d_vn_rec;
     g.d_all_cn = d.d_all_cn;
     g.d_edge_rec = d.d_edge_rec;
     g.d_vn_pos = d.d_vn_pos;
+    g.d_vn_hold = d.d_vn_hold;
   }
   const auto& sh = s->impl->host;
   g.per_frame = sh.per_frame;
@@ -1043,7 +1045,7 @@ int ldpcb_decode_plan(ldpcb_code code, ldpcb_schedule s, int64_t frames, int32_t
   return guard([&] {
     const auto g = dev_graph(code, s);
     const auto p = ldpcb::plan_decode(g, frames);
-    if (kernel) *kernel = p.kernel == 1 ? 10 + p.fv : (p.kernel == 3 ? 20 + p.fpc / 2 : p.kernel);
+    if (kernel) *kernel = p.kernel == 1 ? 10 + p.fv : (p.kernel == 3 ? 20 + p.fv : p.kernel);
     if (fpc) *fpc = p.fpc;
     if (threads) *threads = p.threads;
     if (smem_bytes) *smem_bytes = p.smem;

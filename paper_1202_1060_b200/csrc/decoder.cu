@@ -1334,7 +1334,7 @@ Plan plan_decode(const DevGraph& g, int64_t frames, bool early_stop) {
   // explicit resident tuning was requested; kernel 3 forces it
   const int force = g_force_kernel.load();
   if (force == 3 ||
-      (force == 0 && g.d_ng > 0 && g_tune_fpc.load() == 0 && g_tune_threads.load() == 0 && g_tune_fv.load() == 0)) {
+      (force == 0 && g.d_fv > 0 && g_tune_fpc.load() == 0 && g_tune_threads.load() == 0 && g_tune_fv.load() == 0)) {
     const Plan d = plan_direct(g, frames);
     if (d.kernel == 3 || force == 3) return d;
   }

@@ -2,23 +2,31 @@
 // degree-6 codes whose VNs have degree <= 3 (BASELINE configs 1, 2, 5: the
 // (3,6) n=1008 code) under schedules whose groups fit one CN item per thread.
 //
-// State per frame pair (two frames per 8-byte cell, host.hpp DirectTables):
-// one c2v cell per edge, one L cell per VN (clamped channel LLR, log2 units).
-// A CN item of group g (decoder.hpp:112-127) forms, for each of its six VNs,
-//     v2c_k = L_v + c2v_a + c2v_b        (var_update, decoder.hpp:91-105)
-// from the OTHER two edges of v, runs the exclusion boxplus (check_update,
-// decoder.hpp:59-87; common.cuh) and overwrites its own six c2v cells. There
-// is no posterior array: nothing is updated in place, no fix-up re-sum and no
-// exact-totals pass exist, and every v2c is exact to two fp32 additions.
-// Posteriors are formed only where the reference forms them: for the hard
-// decision / syndrome test (decoder.hpp:162-171) and the outputs.
+// State of the FV frames a CTA decodes (host.hpp DirectTables): one array of
+// cells of FV floats (one per frame) -- a cell per edge and an L cell per VN
+// (clamped channel LLR, log2 units). Every VN has one holder edge whose cell
+// stores c2v + L; every CN holds exactly two. A CN item of group g
+// (decoder.hpp:112-127) forms the v2c of its six edges (var_update,
+// decoder.hpp:91-105) as
+//     holder edge   v2c = (c2v_x + c2v_y) + L          three reads
+//     other edges   v2c = (c2v_h + L) + c2v_o          two reads
+// runs the exclusion boxplus (check_update, decoder.hpp:59-87; common.cuh) and
+// overwrites its own six cells (c2v, or c2v + L for the two it holds): 14
+// reads and 6 writes of shared memory per CN. There is no posterior array:
+// nothing is updated in place, no fix-up re-sum and no exact-totals pass
+// exist, and every v2c is exact to two fp32 additions. Posteriors are formed
+// only where the reference forms them: for the hard decision / syndrome test
+// (decoder.hpp:162-171) and the outputs.
+//
+// A thread serves all FV frames of its CN: one 16-byte (FV = 4) or 8-byte
+// shared-memory access per cell, every add / mul / fma as packed fp32 on frame
+// pairs (common.cuh boxplus_row_x2), and with FV = 4 two independent boxplus
+// chains per thread, which fills the fixed-latency gaps a single chain leaves
+// and halves the per-frame cost of records, addresses and barriers.
 //
 // Jacobi inside a group: a CN of the group may read a cell that another CN of
-// the same group overwrites (a VN shared by both). Every thread therefore
-// arrives on an mbarrier once its own loads have returned and waits on it
-// right before its first store -- by then (hundreds of cycles of boxplus
-// later) all loads of the group have long been issued, so the wait costs
-// nothing -- and one __syncthreads per group orders the stores before the
+// the same group overwrites (a VN shared by both), so one barrier separates
+// the loads of a group from its stores and a second one the stores from the
 // next group's loads. A group is one CN item per thread (the launch plan
 // guarantees it), so no item of a group can start after another has stored.
 //
@@ -29,6 +37,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -42,376 +51,433 @@ namespace {
 
 using namespace dev;
 
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-// `tie` is a value the wait must follow in program order (the first boxplus
-// output): without it the compiler hoists the wait above the arithmetic.
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, f32x2& tie) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "LDPCB_WAIT:\n"
-      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      "@p bra LDPCB_DONE;\n"
-      "bra LDPCB_WAIT;\n"
-      "LDPCB_DONE:\n"
-      "}\n"
-      : "+l"(tie)
-      : "r"(bar), "r"(parity)
-      : "memory");
+constexpr int kDirectThreads = 96;  // C1 NDGSBP: 84 CN items per group
+
+// The CTA's dynamic shared memory: the cell array, then the hard-decision
+// bytes. Every device function addresses it
+// through this symbol (a pointer parameter would lose the shared-window base
+// and cost an address add per access).
+extern __shared__ __align__(16) char dsm[];
+
+// resident CTAs per SM the register budget is sized for: shared memory fits
+// six 2-frame CTAs (33 KB) or three 4-frame CTAs (66 KB). A seventh 2-frame
+// CTA was tried (all control state moved to global memory so that the
+// kernel's shared memory is exactly the 32256-byte state): the 16 K registers
+// of an SM sub-partition hold five 96-register warps, so 21 warps per SM need
+// 80 registers per thread, and that build (64 bytes of spills) ran 4 % slower
+// than six CTAs (108.3 against 104.1 ms per 2^21 frames).
+template <int FV>
+constexpr int direct_min_blocks() {
+  return FV == 2 ? 6 : 3;
 }
 
-template <int NG>
-struct DirectCfg {
-  static constexpr int kMaxThreads = NG == 1 ? 96 : (NG == 2 ? 192 : 256);
-  static constexpr int kMinBlocks = NG == 1 ? 6 : (NG == 2 ? 3 : 2);
+// one cell: FV frames as FV / 2 packed pairs
+template <int FV>
+struct Cell {
+  f32x2 p[FV / 2];
 };
+template <int FV>
+__device__ __forceinline__ Cell<FV> ld_cell(const char* base, uint32_t off) {
+  Cell<FV> r;
+  if constexpr (FV == 4) {
+    const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(base + off);
+    r.p[0] = t.x;
+    r.p[1] = t.y;
+  } else {
+    r.p[0] = *reinterpret_cast<const f32x2*>(base + off);
+  }
+  return r;
+}
+template <int FV>
+__device__ __forceinline__ void st_cell(char* base, uint32_t off, const Cell<FV>& c) {
+  if constexpr (FV == 4)
+    *reinterpret_cast<ulonglong2*>(base + off) = make_ulonglong2(c.p[0], c.p[1]);
+  else
+    *reinterpret_cast<f32x2*>(base + off) = c.p[0];
+}
+template <int FV>
+__device__ __forceinline__ Cell<FV> add_cell(const Cell<FV>& a, const Cell<FV>& b) {
+  Cell<FV> r;
+#pragma unroll
+  for (int i = 0; i < FV / 2; ++i) r.p[i] = add2(a.p[i], b.p[i]);
+  return r;
+}
+// bit i = sign of frame i (tie -> 0, decoder.hpp:166)
+template <int FV>
+__device__ __forceinline__ unsigned sign_bits(const Cell<FV>& t) {
+  unsigned b = 0;
+#pragma unroll
+  for (int i = 0; i < FV / 2; ++i)
+    b |= ((lo2(t.p[i]) < 0.f ? 1u : 0u) | (hi2(t.p[i]) < 0.f ? 2u : 0u)) << (2 * i);
+  return b;
+}
 
-// the twelve words of a CN record (host.hpp DirectTables)
+// the ten words of a CN record (host.hpp DirectTables), prefetched into
+// registers one group ahead
 struct DRec {
-  int4 a, b, c;
+  int4 a, b;
+  int2 c;
   __device__ __forceinline__ void load(const int32_t* __restrict__ p) {
     const int4* q = reinterpret_cast<const int4*>(p);
     a = __ldg(q);
     b = __ldg(q + 1);
-    c = __ldg(q + 2);
+    c = __ldg(reinterpret_cast<const int2*>(q + 2));
   }
+  // keeps the consumers of the prefetched record below this point
   __device__ __forceinline__ void pin() {
     asm volatile("" : "+r"(a.x), "+r"(a.y), "+r"(a.z), "+r"(a.w));
     asm volatile("" : "+r"(b.x), "+r"(b.y), "+r"(b.z), "+r"(b.w));
-    asm volatile("" : "+r"(c.x), "+r"(c.y), "+r"(c.z), "+r"(c.w));
+    asm volatile("" : "+r"(c.x), "+r"(c.y));
   }
 };
 
-__device__ __forceinline__ f32x2 ldc(const char* base, uint32_t off) {
-  return *reinterpret_cast<const f32x2*>(base + off);
-}
 __device__ __forceinline__ uint32_t lo16(int w) { return static_cast<uint32_t>(w) & 0xffffu; }
 __device__ __forceinline__ uint32_t hi16(int w) { return static_cast<uint32_t>(w) >> 16; }
 
-// SPLIT: the split arrive / wait barrier described above; otherwise a plain
-// __syncthreads between the loads and the boxplus (A/B).
-template <int NG, bool SPLIT>
-__global__ void __launch_bounds__(DirectCfg<NG>::kMaxThreads, DirectCfg<NG>::kMinBlocks)
-    decode_direct(const DevGraph g, const DecodeArgs a, unsigned long long* queue) {
-  constexpr int FPC = 2 * NG;
-  extern __shared__ __align__(16) char dsm[];
-  __shared__ long long s_frame[FPC];
-  __shared__ int s_done[FPC], s_weight[FPC], s_iters[FPC], s_conv[FPC], s_berr[FPC];
-  __shared__ unsigned long long s_cnt[6];
-  __shared__ __align__(8) unsigned long long s_bar;
-  __shared__ int s_active, s_retiring;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int n = g.n, m = g.m, E = g.E;
-  const uint32_t pair_bytes = static_cast<uint32_t>(g.d_cells) * 8u;
-  const uint32_t l_off = static_cast<uint32_t>(g.d_l_base) * 8u;
-  const int npad = (n + 15) & ~15;
-  uint8_t* const s_hd = reinterpret_cast<uint8_t*>(dsm + NG * pair_bytes);  // [NG][npad] sign bits, bit h = frame h
-  int2* const s_go = reinterpret_cast<int2*>(dsm + NG * pair_bytes + ((NG * npad + 15) & ~15));
-  const int nb = (n + 7) >> 3;
-  const uint32_t bar = smem_addr(&s_bar);
-  const bool check = a.early_stop || a.trace;
-  const bool dump = a.max_subiters > 0;
-
-  // slot ff = frame half h = ff & 1 of pair ff >> 1
-  auto slot_base = [&](int ff) { return dsm + (ff >> 1) * pair_bytes + (ff & 1) * 4; };
-  // init_state (decoder.hpp:39-52): L = clamp(llr), every c2v = 0 (f < 0: idle slot)
-  auto load_slot = [&](int ff, long long f) {
-    char* const sb = slot_base(ff);
-    if (f >= 0) {
-      const float* llr = a.llr + f * n;
-      if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(a.llr) & 15) == 0) {
-        const float4* l4 = reinterpret_cast<const float4*>(llr);
-        for (int b = tid; b < n / 4; b += nt) {
-          const float4 x = __ldg(l4 + b);
-          const int4 p = __ldg(reinterpret_cast<const int4*>(g.d_vn_pos) + b);
-          *reinterpret_cast<float*>(sb + l_off + p.x * 8) = clamp_llr(x.x) * kLog2e;
-          *reinterpret_cast<float*>(sb + l_off + p.y * 8) = clamp_llr(x.y) * kLog2e;
-          *reinterpret_cast<float*>(sb + l_off + p.z * 8) = clamp_llr(x.z) * kLog2e;
-          *reinterpret_cast<float*>(sb + l_off + p.w * 8) = clamp_llr(x.w) * kLog2e;
-        }
-      } else {
-        for (int i = tid; i < n; i += nt)
-          *reinterpret_cast<float*>(sb + l_off + __ldg(g.d_vn_pos + i) * 8) = clamp_llr(__ldg(llr + i)) * kLog2e;
-      }
-      if (a.trace)
-        for (int i = tid; i < a.max_iters; i += nt) a.trace[f * a.max_iters + i] = -1;
+// One sub-iteration (decoder.hpp:112-127): the thread's CN item of group grp.
+// cn: the CNs of this group; next_rec: the thread's record for this group
+// (requested one group ahead). On return they describe the next group.
+template <int FV>
+__device__ __forceinline__ void direct_group(const DevGraph& g, int tid, int grp, int& cn, DRec& next_rec) {
+  const int G = g.G;
+  const bool has = tid < cn;
+  Cell<FV> x[6], lh[2];
+  uint32_t own[6];
+  const DRec cur = next_rec;
+  if (has) {
+    const int4 ra = cur.a, rb = cur.b;
+    const int2 rc = cur.c;
+    const int w[10] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w, rc.x, rc.y};
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {  // the two edges this CN holds: (c2v_x + c2v_y) + L
+      own[k] = lo16(w[2 * k]);
+      const Cell<FV> cx = ld_cell<FV>(dsm, hi16(w[2 * k]));
+      const Cell<FV> cy = ld_cell<FV>(dsm, lo16(w[2 * k + 1]));
+      lh[k] = ld_cell<FV>(dsm, hi16(w[2 * k + 1]));
+      x[k] = add_cell<FV>(add_cell<FV>(cx, cy), lh[k]);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {  // (c2v_h + L) + c2v_o: the holder's cell and the third edge's
+      auto field = [&](int i) { return (i & 1) ? hi16(w[4 + i / 2]) : lo16(w[4 + i / 2]); };
+      own[2 + j] = field(3 * j);
+      x[2 + j] = add_cell<FV>(ld_cell<FV>(dsm, field(3 * j + 1)), ld_cell<FV>(dsm, field(3 * j + 2)));
+    }
+  }
+  // the next group's record, requested behind this group's shared-memory
+  // loads a whole group before use
+  const int gn = grp + 1 < G ? grp + 1 : 0;
+  const int n0 = g.d_goff[gn], ncn = g.d_goff[gn + 1] - n0;
+  if (tid < ncn) next_rec.load(g.d_cn_rec + static_cast<size_t>(n0 + tid) * 12);
+  __syncthreads();  // every load of the group precedes every store
+  if (has) {
+    if constexpr (FV == 2) {  // every output stored as the boxplus emits it
+      f32x2 xi[6];
+#pragma unroll
+      for (int k = 0; k < 6; ++k) xi[k] = x[k].p[0];
+      boxplus_row_x2<6, true>(xi, 6, [&](int k, f32x2 c) {
+        *reinterpret_cast<f32x2*>(dsm + own[k]) = k < 2 ? add2(c, lh[k].p[0]) : c;
+      });
     } else {
-      for (int i = tid; i < n; i += nt) *reinterpret_cast<float*>(sb + l_off + i * 8) = kClampB;
+      Cell<FV> out[6];
+#pragma unroll
+      for (int i = 0; i < FV / 2; ++i) {
+        f32x2 xi[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) xi[k] = x[k].p[i];
+        boxplus_row_x2<6, true>(xi, 6, [&](int k, f32x2 c) { out[k].p[i] = c; });
+      }
+#pragma unroll
+      for (int k = 0; k < 6; ++k) st_cell<FV>(dsm, own[k], k < 2 ? add_cell<FV>(out[k], lh[k]) : out[k]);
     }
-    for (int i = tid; i < g.d_l_base; i += nt) *reinterpret_cast<float*>(sb + i * 8) = 0.f;
-  };
-  auto pull = [&]() -> long long {
-    const unsigned long long f = atomicAdd(queue, 1ull);
-    return f < static_cast<unsigned long long>(a.frames) ? static_cast<long long>(f) : -1ll;
-  };
-
-  if (tid < FPC) {
-    s_frame[tid] = pull();
-    s_done[tid] = s_frame[tid] < 0;
-    s_weight[tid] = s_iters[tid] = s_conv[tid] = s_berr[tid] = 0;
-  }
-  if (tid < 6) s_cnt[tid] = 0ull;
-  if (tid == 0) mbar_init(bar, nt);
-  for (int i = tid; i < g.G; i += nt) s_go[i] = make_int2(__ldg(g.d_cn_off + i), __ldg(g.d_cn_off + i + 1));
-  {  // every cell zero (the zero cell and the padding cells stay zero)
-    float4* z = reinterpret_cast<float4*>(dsm);
-    for (int i = tid; i < static_cast<int>(NG * pair_bytes / 16); i += nt) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   __syncthreads();
-  {
-    bool any = false;
-    for (int ff = 0; ff < FPC; ++ff) any |= s_frame[ff] >= 0;
-    if (!any) return;  // the queue was empty when this CTA started
+  next_rec.pin();
+  cn = ncn;
+}
+
+// Per-CTA control state (shared memory): slot ff holds frame `frame[ff]`
+// (-1: none); done: 0 decoding, 1 idle, 2 retiring, 3 refilled this round.
+template <int FV>
+struct DirectCtl {
+  long long frame[FV];
+  int done[FV], weight[FV], iters[FV], conv[FV], berr[FV];
+  unsigned long long cnt[6];
+  int active, retiring;
+};
+
+__device__ __forceinline__ long long direct_pull(unsigned long long* queue, int64_t frames) {
+  const unsigned long long f = atomicAdd(queue, 1ull);
+  return f < static_cast<unsigned long long>(frames) ? static_cast<long long>(f) : -1ll;
+}
+
+// init_state (decoder.hpp:39-52) of the slots in `mask`: every cell 0
+// (c2v = 0), then L = clamp(llr) (kClampB for an idle slot) into the L cells
+// and the holder cells (0 + L). All global loads of a batch of elements are
+// issued before any is used. The iteration-boundary functions are kept out
+// of line: the sub-iteration loop then owns the whole register budget.
+template <int FV>
+__device__ __forceinline__ void direct_load_slots(const DevGraph& g, const DecodeArgs& a, const DirectCtl<FV>* ctl,
+                                                  unsigned mask) {
+  constexpr int CB = 4 * FV;
+  const int tid = threadIdx.x, nt = blockDim.x, n = g.n;
+  const uint32_t l_off = static_cast<uint32_t>(g.d_l_base) * CB;
+  if (mask == (1u << FV) - 1) {
+    Cell<FV> z;
+#pragma unroll
+    for (int i = 0; i < FV / 2; ++i) z.p[i] = 0ull;
+    for (int i = tid; i < g.d_l_base; i += nt) st_cell<FV>(dsm, i * CB, z);
+  } else {
+#pragma unroll
+    for (int ff = 0; ff < FV; ++ff)
+      if (mask & (1u << ff))
+        for (int i = tid; i < g.d_l_base; i += nt) *reinterpret_cast<float*>(dsm + 4 * ff + i * CB) = 0.f;
   }
-  for (int ff = 0; ff < FPC; ++ff) load_slot(ff, s_frame[ff]);
   __syncthreads();
-
-  // this thread's item of a group with cn CNs: pair p = tid / cn, CN j = tid % cn
-  auto item_of = [&](int cn, int& p, int& j) {
-    p = 0;
-    j = tid;
-    if constexpr (NG >= 2)
-      if (j >= cn) j -= cn, p = 1;
-    if constexpr (NG >= 3)
-      if (j >= cn) j -= cn, p = 2;
-    return j < cn;
-  };
-  DRec next_rec;
-  int2 go = s_go[0];
-  {
-    int p, j;
-    if (item_of(go.y - go.x, p, j)) next_rec.load(g.d_cn_rec + static_cast<size_t>(go.x + j) * 12);
+  const bool vec = (n & 3) == 0 && (reinterpret_cast<uintptr_t>(a.llr) & 15) == 0;
+  constexpr int U = 3;
+#pragma unroll
+  for (int ff = 0; ff < FV; ++ff) {
+    if (!(mask & (1u << ff))) continue;
+    char* const sb = dsm + 4 * ff;
+    const long long f = ctl->frame[ff];
+    auto put = [&](int pos, int hold, float raw) {
+      const float y = f >= 0 ? clamp_llr(raw) * kLog2e : kClampB;
+      *reinterpret_cast<float*>(sb + l_off + pos * CB) = y;
+      *reinterpret_cast<float*>(sb + hold) = y;
+    };
+    if (f >= 0 && vec) {
+      const float4* l4 = reinterpret_cast<const float4*>(a.llr + f * n);
+      const int4* p4 = reinterpret_cast<const int4*>(g.d_vn_pos);
+      const int4* h4 = reinterpret_cast<const int4*>(g.d_vn_hold);
+      for (int b0 = tid; b0 < n / 4; b0 += U * nt) {
+        float4 x[U];
+        int4 p[U], h[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (b0 + u * nt < n / 4)
+            x[u] = __ldg(l4 + b0 + u * nt), p[u] = __ldg(p4 + b0 + u * nt), h[u] = __ldg(h4 + b0 + u * nt);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (b0 + u * nt < n / 4) {
+            put(p[u].x, h[u].x, x[u].x);
+            put(p[u].y, h[u].y, x[u].y);
+            put(p[u].z, h[u].z, x[u].z);
+            put(p[u].w, h[u].w, x[u].w);
+          }
+      }
+    } else {
+      const float* llr = a.llr + (f >= 0 ? f : 0) * n;
+      for (int i = tid; i < n; i += nt)
+        put(__ldg(g.d_vn_pos + i), __ldg(g.d_vn_hold + i), f >= 0 ? __ldg(llr + i) : 0.f);
+    }
+    if (f >= 0 && a.trace)
+      for (int i = tid; i < a.max_iters; i += nt) a.trace[f * a.max_iters + i] = -1;
   }
-  uint32_t parity = 0;
-  int it_cta = 0, sub = 0;
+  __syncthreads();
+}
 
-  for (;;) {
-    // one iteration for every slot (decoder.hpp:157-160)
-    for (int grp = 0; grp < g.G; ++grp) {
-      if (dump && sub == a.max_subiters) goto dump_state;
-      ++sub;
-      const int cn = go.y - go.x;
-      const int2 ngo = s_go[grp + 1 < g.G ? grp + 1 : 0];
-      int p, j;
-      const bool has = item_of(cn, p, j);
-      const char* const pb = dsm + p * pair_bytes;
-      const DRec cur = next_rec;
-      {  // the next group's record, a whole group before it is needed
-        int pn, jn;
-        if (item_of(ngo.y - ngo.x, pn, jn)) next_rec.load(g.d_cn_rec + static_cast<size_t>(ngo.x + jn) * 12);
-      }
-      f32x2 x[6];
-      uint32_t own[6];
-      if (has) {
-        const int w[12] = {cur.a.x, cur.a.y, cur.a.z, cur.a.w, cur.b.x, cur.b.y,
-                           cur.b.z, cur.b.w, cur.c.x, cur.c.y, cur.c.z, cur.c.w};
+// End of an iteration that tests the syndrome: hard decisions, syndrome
+// weights, per-frame bookkeeping (decoder.hpp:162-177), outputs of the frames
+// that stopped (sim.hpp:119-123) and their refill from the queue.
+// it_cta: iterations since the CTA's slots were last refilled together (fixed
+// iteration counts). Returns 0: carry on, 1: slots were refilled, 2: no slot
+// is busy and the queue is empty.
+template <int FV>
+__device__ __forceinline__ int direct_iteration_end(const DevGraph& g, const DecodeArgs& a,
+                                                    unsigned long long* queue, DirectCtl<FV>* ctl, int it_cta) {
+  constexpr int CB = 4 * FV;
+  const int tid = threadIdx.x, nt = blockDim.x, n = g.n, m = g.m;
+  uint8_t* const s_hd = reinterpret_cast<uint8_t*>(dsm + static_cast<size_t>(g.d_cells) * CB);  // [n] bit i = frame i
+  const int nb = (n + 7) >> 3;
+  const bool check = a.early_stop || a.trace;
+  // hard decisions (tie -> 0) from the totals ((c2v_h + L) + c2v) + c2v, one sign bit per frame
+  for (int pos = tid; pos < n; pos += nt) {
+    const int2 r = __ldg(reinterpret_cast<const int2*>(g.d_vn_rec) + pos);
+    Cell<FV> t = add_cell<FV>(ld_cell<FV>(dsm, lo16(r.x)), ld_cell<FV>(dsm, hi16(r.x)));
+    t = add_cell<FV>(t, ld_cell<FV>(dsm, lo16(r.y)));
+    s_hd[pos] = static_cast<uint8_t>(sign_bits<FV>(t));
+  }
+  __syncthreads();
+  {  // syndrome weight (decoder.hpp:129-137)
+    int w[FV] = {};
+    for (int r = tid; r < m; r += nt) {
+      const int4 q = __ldg(reinterpret_cast<const int4*>(g.d_all_cn) + r);
+      const unsigned x = s_hd[lo16(q.x)] ^ s_hd[hi16(q.x)] ^ s_hd[lo16(q.y)] ^ s_hd[hi16(q.y)] ^ s_hd[lo16(q.z)] ^
+                         s_hd[hi16(q.z)];
 #pragma unroll
-        for (int k = 0; k < 6; ++k) {
-          own[k] = lo16(w[2 * k]);
-          const f32x2 l = ldc(pb, hi16(w[2 * k]));
-          const f32x2 ca = ldc(pb, lo16(w[2 * k + 1]));
-          const f32x2 cb = ldc(pb, hi16(w[2 * k + 1]));
-          x[k] = add2(add2(l, ca), cb);
-        }
-      }
-      if constexpr (SPLIT) {
-        mbar_arrive(bar);  // release: ordered after this thread's loads above
-      } else {
-        __syncthreads();
-      }
-      if (has) {
-        boxplus_row_x2<6, true>(x, 6, [&](int k, f32x2 c) {
-          if constexpr (SPLIT)
-            if (k == 5) mbar_wait(bar, parity, c);  // the first output: every load of the group is done
-          *reinterpret_cast<f32x2*>(const_cast<char*>(pb) + own[k]) = c;
-        });
-      }
-      parity ^= 1u;
-      __syncthreads();
-      next_rec.pin();
-      go = ngo;
+      for (int i = 0; i < FV; ++i) w[i] += (x >> i) & 1u;
     }
-    if (dump) continue;
-    ++it_cta;
-    if (!check && it_cta < a.max_iters) continue;
-    // ---- hard decisions (tie -> 0) from the totals L + sum c2v in ascending
-    // CN order (decoder.hpp:162-166), one sign bit per frame in s_hd
-    for (int i = tid; i < NG * n; i += nt) {
-      const int p = NG == 1 ? 0 : i / n, pos = i - p * n;
-      const char* const pb = dsm + p * pair_bytes;
-      const int2 r = __ldg(reinterpret_cast<const int2*>(g.d_vn_rec) + pos);
-      f32x2 t = ldc(pb, l_off + pos * 8);
-      t = add2(t, ldc(pb, lo16(r.x)));
-      t = add2(t, ldc(pb, hi16(r.x)));
-      t = add2(t, ldc(pb, lo16(r.y)));
-      s_hd[p * npad + pos] = static_cast<uint8_t>((lo2(t) < 0.f ? 1u : 0u) | (hi2(t) < 0.f ? 2u : 0u));
-    }
-    __syncthreads();
-    // ---- syndrome weight (decoder.hpp:129-137)
 #pragma unroll
-    for (int p = 0; p < NG; ++p) {
-      int w0 = 0, w1 = 0;
-      const uint8_t* hd = s_hd + p * npad;
-      for (int r = tid; r < m; r += nt) {
-        const int4 q = __ldg(reinterpret_cast<const int4*>(g.d_all_cn) + r);
-        const unsigned x = hd[lo16(q.x)] ^ hd[hi16(q.x)] ^ hd[lo16(q.y)] ^ hd[hi16(q.y)] ^ hd[lo16(q.z)] ^ hd[hi16(q.z)];
-        w0 += x & 1u;
-        w1 += (x >> 1) & 1u;
-      }
-      if (w0) atomicAdd(&s_weight[2 * p], w0);
-      if (w1) atomicAdd(&s_weight[2 * p + 1], w1);
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int retiring = 0;
-      for (int ff = 0; ff < FPC; ++ff) {
-        if (s_done[ff]) continue;
-        const int w = s_weight[ff];
-        const int it = check ? ++s_iters[ff] : (s_iters[ff] = it_cta);
-        if (a.trace) a.trace[s_frame[ff] * a.max_iters + it - 1] = w;
-        s_conv[ff] = w == 0;
+    for (int i = 0; i < FV; ++i)
+      if (w[i]) atomicAdd(&ctl->weight[i], w[i]);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int retiring = 0, active = 0;
+    for (int ff = 0; ff < FV; ++ff) {
+      if (!ctl->done[ff]) {
+        const int w = ctl->weight[ff];
+        const int it = check ? ++ctl->iters[ff] : (ctl->iters[ff] = it_cta);
+        if (a.trace) a.trace[ctl->frame[ff] * a.max_iters + it - 1] = w;
+        ctl->conv[ff] = w == 0;
         if ((w == 0 && a.early_stop) || it >= a.max_iters) {  // decoder.hpp:173-177
-          s_done[ff] = 2;                                       // retiring
+          ctl->done[ff] = 2;
           ++retiring;
         }
       }
-      int active = 0;
-      for (int ff = 0; ff < FPC; ++ff) {
-        s_weight[ff] = 0;
-        active += s_done[ff] != 1;
-      }
-      s_retiring = retiring;
-      s_active = active;
+      ctl->weight[ff] = 0;
+      active += ctl->done[ff] != 1;
     }
-    __syncthreads();
-    if (s_retiring == 0) {
-      if (s_active == 0) break;
-      continue;
-    }
-    // ---- outputs of the frames that stopped (sim.hpp:119-123), then refill
-    for (int ff = 0; ff < FPC; ++ff) {
-      if (s_done[ff] != 2) continue;
-      const long long f = s_frame[ff];
-      const uint8_t* hd = s_hd + (ff >> 1) * npad;
-      const int h = ff & 1;
-      int errs = 0;
-      if (a.bits && a.bits_packed) {
-        for (int b = tid; b < nb; b += nt) {
-          unsigned byte = 0;
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int v = b * 8 + q;
-            if (v < n) byte |= ((hd[__ldg(g.d_vn_pos + v)] >> h) & 1u) << q;
-          }
-          a.bits[f * nb + b] = static_cast<uint8_t>(byte);
-          errs += __popc(byte);
-        }
-      } else if (a.bits || a.counters || a.bit_errors) {
-        for (int v = tid; v < n; v += nt) {
-          const int bit = (hd[__ldg(g.d_vn_pos + v)] >> h) & 1;
-          if (a.bits) a.bits[f * n + v] = static_cast<uint8_t>(bit);
-          errs += bit;
-        }
-      }
-      if (errs) atomicAdd(&s_berr[ff], errs);
-      if (a.posterior) {
-        const char* const sb = slot_base(ff);
-        for (int v = tid; v < n; v += nt) {
-          const int pos = __ldg(g.d_vn_pos + v);
-          const int2 r = __ldg(reinterpret_cast<const int2*>(g.d_vn_rec) + pos);
-          float t = *reinterpret_cast<const float*>(sb + l_off + pos * 8);
-          t += *reinterpret_cast<const float*>(sb + lo16(r.x));
-          t += *reinterpret_cast<const float*>(sb + hi16(r.x));
-          t += *reinterpret_cast<const float*>(sb + lo16(r.y));
-          a.posterior[f * n + v] = t * kLn2;
-        }
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      for (int ff = 0; ff < FPC; ++ff) {
-        if (s_done[ff] != 2) continue;
-        const long long f = s_frame[ff];
-        const int it = s_iters[ff];
-        if (a.iterations) a.iterations[f] = a.early_stop ? it : a.max_iters;
-        if (a.converged) a.converged[f] = static_cast<uint8_t>(s_conv[ff]);
-        if (a.bit_errors) a.bit_errors[f] = s_berr[ff];
-        s_cnt[0] += 1;
-        s_cnt[1] += s_berr[ff];
-        s_cnt[2] += s_berr[ff] > 0;
-        s_cnt[3] += s_conv[ff];
-        s_cnt[4] += a.early_stop ? it : a.max_iters;
-        s_cnt[5] += s_conv[ff] ? (a.early_stop ? it : a.max_iters) : 0;
-        s_frame[ff] = pull();
-        s_done[ff] = s_frame[ff] < 0 ? 1 : 3;  // 3: refilled this round
-        s_iters[ff] = s_conv[ff] = s_berr[ff] = 0;
-      }
-      int active = 0;
-      for (int ff = 0; ff < FPC; ++ff) active += s_done[ff] != 1;
-      s_active = active;
-    }
-    __syncthreads();
-    for (int ff = 0; ff < FPC; ++ff)
-      if (s_done[ff] == 3) load_slot(ff, s_frame[ff]);
-    __syncthreads();
-    if (tid < FPC && s_done[tid] == 3) s_done[tid] = 0;
-    it_cta = 0;
-    if (s_active == 0) break;
-    __syncthreads();
+    ctl->retiring = retiring;
+    ctl->active = active;
   }
-  if (tid == 0 && a.counters)
-    for (int i = 0; i < 6; ++i)
-      if (s_cnt[i]) atomicAdd(a.counters + i, s_cnt[i]);
-  return;
-
-dump_state:
-  // state after max_subiters sub-iterations: c2v and v2c per CN-major edge id
   __syncthreads();
-  for (int ff = 0; ff < FPC; ++ff) {
-    const long long f = s_frame[ff];
+  if (ctl->retiring == 0) return ctl->active == 0 ? 2 : 0;
+  for (int ff = 0; ff < FV; ++ff) {
+    if (ctl->done[ff] != 2) continue;
+    const long long f = ctl->frame[ff];
+    int errs = 0;
+    if (a.bits && a.bits_packed) {
+      for (int b = tid; b < nb; b += nt) {
+        unsigned byte = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int v = b * 8 + q;
+          if (v < n) byte |= ((s_hd[__ldg(g.d_vn_pos + v)] >> ff) & 1u) << q;
+        }
+        a.bits[f * nb + b] = static_cast<uint8_t>(byte);
+        errs += __popc(byte);
+      }
+    } else if (a.bits || a.counters || a.bit_errors) {
+      for (int v = tid; v < n; v += nt) {
+        const int bit = (s_hd[__ldg(g.d_vn_pos + v)] >> ff) & 1;
+        if (a.bits) a.bits[f * n + v] = static_cast<uint8_t>(bit);
+        errs += bit;
+      }
+    }
+    if (errs) atomicAdd(&ctl->berr[ff], errs);
+    if (a.posterior) {
+      const char* const sb = dsm + 4 * ff;
+      for (int v = tid; v < n; v += nt) {
+        const int2 r = __ldg(reinterpret_cast<const int2*>(g.d_vn_rec) + __ldg(g.d_vn_pos + v));
+        float t = *reinterpret_cast<const float*>(sb + lo16(r.x)) + *reinterpret_cast<const float*>(sb + hi16(r.x));
+        t += *reinterpret_cast<const float*>(sb + lo16(r.y));
+        a.posterior[f * n + v] = t * kLn2;
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int active = 0;
+    for (int ff = 0; ff < FV; ++ff) {
+      if (ctl->done[ff] == 2) {
+        const long long f = ctl->frame[ff];
+        const int it = a.early_stop ? ctl->iters[ff] : a.max_iters;
+        if (a.iterations) a.iterations[f] = it;
+        if (a.converged) a.converged[f] = static_cast<uint8_t>(ctl->conv[ff]);
+        if (a.bit_errors) a.bit_errors[f] = ctl->berr[ff];
+        ctl->cnt[0] += 1;
+        ctl->cnt[1] += ctl->berr[ff];
+        ctl->cnt[2] += ctl->berr[ff] > 0;
+        ctl->cnt[3] += ctl->conv[ff];
+        ctl->cnt[4] += it;
+        ctl->cnt[5] += ctl->conv[ff] ? it : 0;
+        ctl->frame[ff] = direct_pull(queue, a.frames);
+        ctl->done[ff] = ctl->frame[ff] < 0 ? 1 : 3;
+        ctl->iters[ff] = ctl->conv[ff] = ctl->berr[ff] = 0;
+      }
+      active += ctl->done[ff] != 1;
+    }
+    ctl->active = active;
+  }
+  __syncthreads();
+  if (ctl->active == 0) return 2;
+  unsigned mask = 0;
+#pragma unroll
+  for (int ff = 0; ff < FV; ++ff) mask |= (ctl->done[ff] == 3 ? 1u : 0u) << ff;
+  direct_load_slots<FV>(g, a, ctl, mask);
+  if (tid < FV && ctl->done[tid] == 3) ctl->done[tid] = 0;
+  __syncthreads();
+  return 1;
+}
+
+// State after a.max_subiters sub-iterations: c2v and v2c per CN-major edge id.
+template <int FV>
+__device__ __forceinline__ void direct_dump(const DevGraph& g, const DecodeArgs& a, const DirectCtl<FV>* ctl) {
+  const int tid = threadIdx.x, nt = blockDim.x, E = g.E;
+  for (int ff = 0; ff < FV; ++ff) {
+    const long long f = ctl->frame[ff];
     if (f < 0) continue;
-    const char* const sb = slot_base(ff);
+    const char* const sb = dsm + 4 * ff;
     for (int e = tid; e < E; e += nt) {
       const int2 r = __ldg(reinterpret_cast<const int2*>(g.d_edge_rec) + e);
-      if (a.c2v_out) a.c2v_out[f * E + e] = *reinterpret_cast<const float*>(sb + lo16(r.x)) * kLn2;
+      const bool holder = hi16(r.x) != 0xffffu;
+      const float l = holder ? *reinterpret_cast<const float*>(sb + hi16(r.x)) : 0.f;
+      // a holder cell stores c2v + L (exact while c2v = 0)
+      if (a.c2v_out) a.c2v_out[f * E + e] = (*reinterpret_cast<const float*>(sb + lo16(r.x)) - l) * kLn2;
       if (a.v2c_out) {
-        float t = *reinterpret_cast<const float*>(sb + hi16(r.x));
-        t += *reinterpret_cast<const float*>(sb + lo16(r.y));
-        t += *reinterpret_cast<const float*>(sb + hi16(r.y));
+        float t = *reinterpret_cast<const float*>(sb + lo16(r.y)) + *reinterpret_cast<const float*>(sb + hi16(r.y));
+        if (holder) t += l;
         a.v2c_out[f * E + e] = clamp_bits(t) * kLn2;
       }
     }
   }
 }
 
+template <int FV>
+__global__ void __launch_bounds__(kDirectThreads, direct_min_blocks<FV>())
+    decode_direct(const DevGraph g, const DecodeArgs a, unsigned long long* queue) {
+  constexpr int CB = 4 * FV;  // cell bytes
+  __shared__ DirectCtl<FV> ctl;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (tid < FV) {
+    ctl.frame[tid] = direct_pull(queue, a.frames);
+    ctl.done[tid] = ctl.frame[tid] < 0;
+    ctl.weight[tid] = ctl.iters[tid] = ctl.conv[tid] = ctl.berr[tid] = 0;
+  }
+  if (tid < 6) ctl.cnt[tid] = 0ull;
+  {  // padding cells stay zero
+    float4* z = reinterpret_cast<float4*>(dsm);
+    for (int i = tid; i < g.d_cells * CB / 16; i += nt) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __syncthreads();
+  {
+    bool any = false;
+#pragma unroll
+    for (int ff = 0; ff < FV; ++ff) any |= ctl.frame[ff] >= 0;
+    if (!any) return;  // the queue was empty when this CTA started
+  }
+  direct_load_slots<FV>(g, a, &ctl, (1u << FV) - 1);
+
+  // the thread's CN record one group ahead
+  int cn = g.d_goff[1] - g.d_goff[0];
+  DRec next_rec;
+  if (tid < cn) next_rec.load(g.d_cn_rec + static_cast<size_t>(g.d_goff[0] + tid) * 12);
+  const bool check = a.early_stop || a.trace;
+  const int G = g.G;
+
+  if (a.max_subiters > 0) {  // state dump
+    for (int sub = 0, grp = 0; sub < a.max_subiters; ++sub, grp = grp + 1 < G ? grp + 1 : 0)
+      direct_group<FV>(g, tid, grp, cn, next_rec);
+    direct_dump<FV>(g, a, &ctl);
+    return;
+  }
+  for (int it_cta = 1;; ++it_cta) {
+    // one iteration for every slot (decoder.hpp:157-160)
+    for (int grp = 0; grp < G; ++grp) direct_group<FV>(g, tid, grp, cn, next_rec);
+    if (!check && it_cta < a.max_iters) continue;
+    const int r = direct_iteration_end<FV>(g, a, queue, &ctl, it_cta);
+    if (r == 2) break;
+    if (r == 1) it_cta = 0;
+  }
+  if (tid == 0 && a.counters)
+    for (int i = 0; i < 6; ++i)
+      if (ctl.cnt[i]) atomicAdd(a.counters + i, ctl.cnt[i]);
+}
+
 using DirectFn = void (*)(const DevGraph, const DecodeArgs, unsigned long long*);
 
-// LDPCB_DIRECT_SPLIT=1 selects the split arrive / wait barrier (A/B: measured
-// 2 % slower than the plain barrier on C1 NDGSBP, 106.9 against 104.5 ms)
-bool split_barrier() {
-  const char* e = std::getenv("LDPCB_DIRECT_SPLIT");
-  return e && std::atoi(e) != 0;
-}
-
-DirectFn pick_direct(int ng) {
-  const bool sp = split_barrier();
-  switch (ng) {
-    case 1: return sp ? decode_direct<1, true> : decode_direct<1, false>;
-    case 2: return sp ? decode_direct<2, true> : decode_direct<2, false>;
-    case 3: return sp ? decode_direct<3, true> : decode_direct<3, false>;
-    default: return nullptr;
-  }
-}
-
-int max_threads_direct(int ng) { return ng == 1 ? 96 : (ng == 2 ? 192 : 256); }
+DirectFn pick_direct(int fv) { return fv == 4 ? decode_direct<4> : (fv == 2 ? decode_direct<2> : nullptr); }
 
 }  // namespace
 
@@ -423,19 +489,19 @@ bool direct_enabled() {
 
 Plan plan_direct(const DevGraph& g, int64_t frames) {
   Plan p;
-  const int ng = g.d_ng;
-  if (ng < 1 || ng > 3 || !g.d_cn_rec || g.per_frame) return p;
-  if (static_cast<long long>(ng) * g.d_max_items > max_threads_direct(ng)) return p;  // one CN item per thread
-  const int npad = (g.n + 15) & ~15;
-  const size_t bytes = static_cast<size_t>(ng) * g.d_cells * 8 + ((ng * npad + 15) & ~15) + 8ull * g.G + 16;
+  const int fv = g.d_fv;
+  if ((fv != 2 && fv != 4) || !g.d_cn_rec || g.per_frame) return p;
+  if (g.d_max_items > kDirectThreads) return p;  // one CN item per thread
+  size_t bytes = static_cast<size_t>(g.d_cells) * 4 * fv + ((g.n + 15) & ~15);
+  if (const char* e = std::getenv("LDPCB_DIRECT_PAD")) bytes += std::atoi(e);  // occupancy experiments
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) optin = 227 * 1024;
   if (bytes + 512 > static_cast<size_t>(optin)) return p;
   p.kernel = 3;
-  p.fpc = 2 * ng;
-  p.fv = 2;
-  p.threads = std::max(64, std::min(max_threads_direct(ng), (ng * g.d_max_items + 31) / 32 * 32));
+  p.fpc = fv;
+  p.fv = fv;
+  p.threads = std::max(64, std::min(kDirectThreads, (g.d_max_items + 31) / 32 * 32));
   p.smem = static_cast<int>(bytes);
   p.degree_bucket = 6;
   p.ctas = (frames + p.fpc - 1) / p.fpc;
@@ -447,30 +513,31 @@ int launch_direct(const DevGraph& g, const DecodeArgs& a, void* stream, Plan* us
   if (used) *used = p;
   if (p.kernel != 3) return static_cast<int>(cudaErrorInvalidConfiguration);
   if (a.frames <= 0) return 0;
-  DirectFn fn = pick_direct(g.d_ng);
+  DirectFn fn = pick_direct(g.d_fv);
   cudaError_t err =
       cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem);
   if (err != cudaSuccess) return static_cast<int>(err);
   // resident CTAs per device (cached per kernel, configuration and device)
   static std::mutex mu;
   static std::map<std::tuple<const void*, int, int, int>, int> cache;
-  int dev = 0, sms = 0, per_sm = 0;
+  int dev = 0, resident = 0;
   cudaGetDevice(&dev);
   {
     std::lock_guard<std::mutex> lk(mu);
     const auto key = std::make_tuple(reinterpret_cast<const void*>(fn), p.threads, p.smem, dev);
     auto it = cache.find(key);
     if (it == cache.end()) {
+      int sms = 0, per_sm = 0;
       if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, p.threads, p.smem) != cudaSuccess || per_sm <= 0)
         return static_cast<int>(cudaErrorInvalidConfiguration);
       it = cache.emplace(key, sms * per_sm).first;
     }
-    per_sm = it->second;  // CTAs per device
+    resident = it->second;
   }
   auto st = static_cast<cudaStream_t>(stream);
-  // state dumps stop every CTA after its first frames: one CTA per FPC frames
-  const int64_t ctas = a.max_subiters > 0 ? p.ctas : std::min<int64_t>(p.ctas, per_sm);
+  // state dumps stop every CTA after its first frames: one CTA per FV frames
+  const int64_t ctas = a.max_subiters > 0 ? p.ctas : std::min<int64_t>(p.ctas, resident);
   unsigned long long* queue = nullptr;
   err = cudaMallocAsync(reinterpret_cast<void**>(&queue), sizeof(unsigned long long), st);
   if (err == cudaSuccess) err = cudaMemsetAsync(queue, 0, sizeof(unsigned long long), st);

@@ -147,28 +147,37 @@ KernelTables kernel_tables(const CodeData& c, const ScheduleData& s, int cs, boo
 
 
 // Tables of the direct (posterior-free) resident kernel (direct.cu) for codes
-// whose VNs have degree <= 3 and whose CNs all have degree 6. A frame pair's
-// state is one array of 8-byte cells (two frames per cell): a c2v cell per
-// edge, an L cell per VN (clamped channel LLR) and one constant-zero cell.
-// A CN item forms v2c_k = L_v + c2v_a + c2v_b from the OTHER two edges of
-// each of its VNs (a < b in CN order; zero cell past the VN's degree), so no
-// posterior array, no in-place update and no fix-up pass exist. Every field is
-// a 16-bit byte offset into the pair's cell array (cells * 8 <= 65536):
-//   CN record  12 ints: word 2k = own_k | L_k << 16, word 2k+1 = a_k | b_k << 16
-//   VN record   2 ints, indexed by VN position: c_0 | c_1 << 16, c_2 (hard decisions)
+// whose VNs all have degree 3 and whose CNs all have degree 6. The state of
+// the fv (2 or 4) frames a CTA decodes is one array of cells of fv floats (one
+// per frame): a cell per edge and an L cell per VN (clamped channel LLR).
+// Every VN has one "holder" edge, chosen so that every CN holds exactly two
+// (a perfect matching): the holder's cell stores c2v + L, the other two
+// edges' cells the plain c2v. A CN item then forms (var_update)
+//   holder edge   v2c = (c2v_x + c2v_y) + L        three reads
+//   other edges   v2c = (c2v_h + L) + c2v_o        two reads (the holder cell and the third edge's)
+// i.e. 14 reads and 6 writes per CN, and no posterior array, in-place update
+// or fix-up pass exist. Every field is a 16-bit byte offset into the cell
+// array (cells * 4 fv <= 65536):
+//   CN record  12 ints (10 used): positions 0, 1 = the CN's holder edges as
+//              own | r0 << 16, r1 | L << 16; then positions 2..5 as the
+//              16-bit triples own, r0, r1 packed two per word
+//   VN record   2 ints, indexed by VN position: holder | second << 16, third
+//              (hard decisions: total = (holder + second) + third)
+//   vn_hold     per VN id: its holder cell (frame refill writes L there)
 //   all_cn      4 ints per CN: the six VN positions as 16-bit fields (syndrome)
-//   edge_rec    2 ints per CN-major edge id, same fields as a CN record (state dumps)
-// Cell ids are bank-coloured (host_direct.cpp): the cells a half-warp touches
-// in one instruction fall in distinct banks where possible.
+//   edge_rec    2 ints per CN-major edge id: own | (holder ? L : 0xffff) << 16, r0 | r1 << 16 (state dumps)
+// Cell ids, record positions and read orders are bank-coloured
+// (host_direct.cpp): the cells a wavefront touches in one instruction fall in
+// distinct banks where possible.
 struct DirectTables {
   bool ok = false;
-  int ng = 1;        // frame pairs per CTA the colouring assumed
-  int cells = 0;     // cells per frame pair, multiple of 16; the last one is the zero cell
+  int fv = 2;        // frames per cell (2: 8-byte cells, 4: 16-byte cells)
+  int cells = 0;     // cells, multiple of 16
   int l_base = 0;    // L cell of position p = l_base + p
   int max_items = 0;
-  std::vector<int32_t> cn_off, cn_rec, vn_rec, all_cn, edge_rec, vn_pos;
+  std::vector<int32_t> cn_off, cn_rec, vn_rec, vn_hold, all_cn, edge_rec, vn_pos;
 };
-DirectTables direct_tables(const CodeData& c, const ScheduleData& s, int ng);
+DirectTables direct_tables(const CodeData& c, const ScheduleData& s, int fv);
 
 ScheduleData schedule_from_groups(const CodeData& c, Kind kind, const Rows& groups);
 ScheduleData flooding_schedule(const CodeData& c);

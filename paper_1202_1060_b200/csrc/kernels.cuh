@@ -33,14 +33,18 @@ struct DevGraph {
   const uint32_t* cn_fresh = nullptr;   // per cn_rec record
   const uint32_t* fix_fresh = nullptr;  // per fix_rec record
   bool covers = false;
-  // direct (posterior-free) kernel tables (host.hpp DirectTables); d_ng = 0: none
-  int d_ng = 0, d_cells = 0, d_l_base = 0, d_max_items = 0;
-  const int32_t* d_cn_off = nullptr;
+  // direct (posterior-free) kernel tables (host.hpp DirectTables); d_fv = 0: none
+  int d_fv = 0, d_cells = 0, d_l_base = 0, d_max_items = 0;
+  // first CN record of every group, a kernel parameter (constant bank): group
+  // ranges then cost a uniform constant load, no vector register
+  static constexpr int kDirectMaxGroups = 96;
+  uint16_t d_goff[kDirectMaxGroups + 1] = {};
   const int32_t* d_cn_rec = nullptr;
   const int32_t* d_vn_rec = nullptr;
   const int32_t* d_all_cn = nullptr;
   const int32_t* d_edge_rec = nullptr;
   const int32_t* d_vn_pos = nullptr;
+  const int32_t* d_vn_hold = nullptr;
   // per-frame random grouping (host.hpp ScheduleData::per_frame)
   bool per_frame = false, regroup = false, balanced = false;
   int nominal = 0, k_overlap = 0, list_slots = 0;

@@ -15,8 +15,5 @@ for l in sys.stdin:
 " || tail -3 gpurun_out/ab_err.log
 }
 EXTRA="--kernel 1"; run resident X=1; EXTRA=""
-for ng in 1 2 3; do
-  for sp in 1 0; do
-    run "direct ng=$ng split=$sp" LDPCB_DIRECT_NG=$ng LDPCB_DIRECT_SPLIT=$sp
-  done
-done
+run "direct staged records" LDPCB_BANK_ITERS=4000
+run "direct register records" LDPCB_BANK_ITERS=4000 LDPCB_LIBRARY=paper_1202_1060_b200/libldpc_b200_regrec.so

@@ -255,7 +255,9 @@ def test_tuning_and_ragged_batches_are_identical(P, torch, orc, fpc, threads):
     s = P.configs.c1_schedules(g)["ndgsbp"]
     llr = cu(torch, orc.transmit_batch_f32(P.sigma2_from_ebn0(1.5, g.rate), 4, g.n_vars, 0, 37, THREADS))
     P.set_tuning(0, 0)
+    P.set_kernel(1)  # the posterior-based resident kernel: its launch shapes are what set_tuning selects
     base = to_np(P.decode_batch(g, s, llr, 20, posterior=True))
+    P.set_kernel(0)
     try:
         P.set_tuning(fpc, threads)
         other = to_np(P.decode_batch(g, s, llr, 20, posterior=True))
@@ -648,3 +650,92 @@ def test_fix16_records_are_bit_identical(P, torch, orc, case):
     for a, b in ((outs[0], outs[2]), (outs[1], outs[3])):
         for k in a:
             assert np.array_equal(a[k], b[k]), k
+
+
+# ----------------------------------------- posterior-free resident kernel ----
+@pytest.mark.parametrize("sched", ["ndgsbp", "gsbp"])
+def test_direct_kernel_is_the_default_and_matches_the_posterior_kernel(P, torch, orc, sched):
+    """C1 under NDGSBP / GSBP decodes on the posterior-free kernel (direct.cu:
+    plan kernel 22); flooding (504 CNs in one group) keeps the posterior-based
+    one. Against that kernel and the reference: >= 99.9 % identical frames
+    with early stop and at fixed 10 iterations, posteriors within 1e-3,
+    identical traces on identical frames, counters equal to the outputs."""
+    g = P.configs.c1_code()
+    sch = P.configs.c1_schedules(g)
+    s = sch[sched]
+    assert P.plan(g, s, 1000)["kernel"] == 22
+    assert P.plan(g, sch["bp"], 1000)["kernel"] == 12
+    F = 6001
+    llr_h = orc.transmit_batch_f32(P.sigma2_from_ebn0(1.75, g.rate), 11, g.n_vars, 0, F, THREADS)
+    llr = cu(torch, llr_h)
+    og = orc.graph(g.n_vars, *g.csr())
+    for es, iters in ((True, 20), (False, 10)):
+        P.set_kernel(1)
+        try:
+            old = to_np(P.decode_batch(g, s, llr, iters, early_stop=es, posterior=True, trace=True))
+        finally:
+            P.set_kernel(0)
+        cnt = torch.zeros(6, dtype=torch.int64, device="cuda")
+        new = to_np(P.decode_batch(g, s, llr, iters, early_stop=es, posterior=True, trace=True, counters=cnt))
+        packed = to_np(P.decode_batch(g, s, llr, iters, early_stop=es, packed=True))
+        assert np.array_equal(np.unpackbits(packed["bits"], axis=1, count=g.n_vars, bitorder="little"), new["bits"])
+        assert np.array_equal(packed["iterations"], new["iterations"])
+        ref = orc.decode_batch(og, s.groups, llr_h, iters, early_stop=es, threads=THREADS, posterior=True)
+        same_old, same_ref = frame_parity(new, old), frame_parity(new, ref)
+        frac, worst = post_stats(new["posterior"], ref["posterior"], same_ref & (ref["converged"] == 1))
+        print(f"direct {sched} es={es}: identical to the posterior kernel {same_old.mean():.5f}, to the reference "
+              f"{same_ref.mean():.5f}, posteriors within 1e-3 {frac:.6f} (max {worst:.2e})")
+        assert same_old.mean() >= 0.999 and same_ref.mean() >= 0.999 and frac >= 0.9999
+        # a rounding-level difference can move one intermediate syndrome weight of a frame that ends identical
+        assert (new["syndrome_trace"] == old["syndrome_trace"]).all(axis=1).mean() >= 0.995
+        be = new["bits"].sum(1)
+        conv = new["converged"] == 1
+        assert cnt.cpu().tolist() == [F, int(be.sum()), int((be > 0).sum()), int(conv.sum()),
+                                      int(new["iterations"].sum()), int(new["iterations"][conv].sum())]
+
+
+def test_direct_kernel_ragged_batches_and_forced_selection(P, torch, orc):
+    """A frame's outputs do not depend on the batch it is decoded in (slots of
+    persistent CTAs are independent lanes); kernel 3 is refused where the
+    schedule does not qualify."""
+    g = P.configs.c1_code()
+    sch = P.configs.c1_schedules(g)
+    s = sch["ndgsbp"]
+    llr = cu(torch, orc.transmit_batch_f32(P.sigma2_from_ebn0(1.5, g.rate), 4, g.n_vars, 0, 2501, THREADS))
+    for es, iters in ((True, 20), (False, 7)):
+        base = to_np(P.decode_batch(g, s, llr, iters, early_stop=es, posterior=True, trace=True))
+        for F in (1, 2, 3, 13, 777):
+            part = to_np(P.decode_batch(g, s, llr[:F].contiguous(), iters, early_stop=es, posterior=True, trace=True))
+            for k in part:
+                assert np.array_equal(part[k], base[k][:F]), (es, F, k)
+    P.set_kernel(3)
+    try:
+        forced = to_np(P.decode_batch(g, s, llr[:64].contiguous(), 20, posterior=True))
+        with pytest.raises(Exception):
+            P.decode_batch(g, sch["bp"], llr[:64].contiguous(), 20)
+    finally:
+        P.set_kernel(0)
+    auto = to_np(P.decode_batch(g, s, llr[:64].contiguous(), 20, posterior=True))
+    for k in auto:
+        assert np.array_equal(auto[k], forced[k]), k
+
+
+def test_direct_kernel_four_frames_per_thread(P, torch, orc):
+    """LDPCB_DIRECT_FV=4 (16-byte cells, two boxplus chains per thread; the
+    tables are built when the schedule handle is made): same bar against the
+    reference, ragged batch included."""
+    os.environ["LDPCB_DIRECT_FV"] = "4"
+    try:
+        g = P.configs.c1_code()
+        s = P.GroupSchedule.windows(g, 8, 84, 63, P.NONDISJOINT)
+    finally:
+        os.environ.pop("LDPCB_DIRECT_FV", None)
+    assert P.plan(g, s, 1000)["kernel"] == 24
+    F = 4003
+    llr_h = orc.transmit_batch_f32(P.sigma2_from_ebn0(2.0, g.rate), 2, g.n_vars, 0, F, THREADS)
+    gpu = to_np(P.decode_batch(g, s, cu(torch, llr_h), 20, posterior=True))
+    ref = orc.decode_batch(orc.graph(g.n_vars, *g.csr()), s.groups, llr_h, 20, early_stop=True, threads=THREADS,
+                           posterior=True)
+    same = frame_parity(gpu, ref)
+    frac, worst = post_stats(gpu["posterior"], ref["posterior"], same & (ref["converged"] == 1))
+    assert same.mean() >= 0.999 and frac >= 0.9999, (same.mean(), frac, worst)
