@@ -747,6 +747,15 @@ void simulate_frames(ldpcb_code code, ldpcb_schedule s, double sigma2, uint64_t 
   if (p0.kernel == 0) throw std::runtime_error("no decoder plan for this code (check degree or memory)");
   auto st = static_cast<cudaStream_t>(stream);
   int64_t chunk = std::max<int64_t>(p0.fpc, (int64_t{256} << 20) / (4 * g.n));
+  if (p0.kernel == 2 && early_stop) {
+    // streamed early stop: frames flow through the frame queue's lanes inside one decode
+    // call, so a chunk holds many lane refills (65536 frames where a sixth of the free
+    // memory holds their LLRs; the lanes' state takes as much again)
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
+    const int64_t fit = static_cast<int64_t>(free_b / 6 / (4ull * g.n));
+    chunk = std::max(chunk, std::min<int64_t>(65536, fit));
+  }
   chunk = std::min<int64_t>(chunk, frames);
   float* scratch = nullptr;
   cuda_check(cudaMallocAsync(&scratch, chunk * g.n * sizeof(float), st), "cudaMallocAsync");

@@ -170,8 +170,11 @@ __global__ void stream_init(int n, const int32_t* __restrict__ pos, const float*
 // first touch), which is what a zeroed c2v and P = L would give.
 // FRESH = false compiles none of the fresh-frame code (the fixed-iteration
 // and chunked early-stop paths: 106 registers, two CTAs per SM; with it 147).
+// Two CTAs per SM: the fresh-frame variant is held to 128 registers as well
+// (92 bytes of spills; at its natural 146 registers one CTA per SM fits and
+// the frame queue's CN launches took 190 us instead of 145).
 template <int D, bool EXACT, int V, bool FRESH>
-__global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ recs, int CS, int count, ChunkState s,
+__global__ void __launch_bounds__(256, (D <= 6 && V == 4) ? 2 : 1) stream_cn(const int32_t* __restrict__ recs, int CS, int count, ChunkState s,
                                                  const uint32_t* __restrict__ fresh) {
   pdl_launch_next();
   const int64_t QB = s.B / V;
@@ -255,6 +258,118 @@ __global__ void __launch_bounds__(256) stream_cn(const int32_t* __restrict__ rec
     }
     stv<V>(s.c2v + static_cast<int64_t>(base + k) * s.B + V * q, o);
     if (mask & (1u << k)) stv<V>(s.P + static_cast<int64_t>(cr.var(k)) * s.B + V * q, p);
+  }
+}
+
+// ---- stream_cn with TMA staging (regular rows of degree 3 / 6, four frames
+// per thread, chunk layouts whose quad count is a multiple of the CTA size).
+// A CTA serves one CN record and kTmaQuads consecutive frame quads: the D
+// posterior rows and D c2v rows it needs are 2 D contiguous 4 KB segments of
+// the [index][B] state, fetched by 2 D bulk copies (cp.async.bulk, the 1-D
+// TMA) that one thread issues against an mbarrier -- no per-thread address
+// arithmetic and no registers holding loads in flight, so three CTAs fit an
+// SM (144 KB of state in flight against 96 KB for the LDG.128 kernel). Every
+// thread then works on its quad in shared memory (packed fp32 on frame
+// pairs, bit-identical to the scalar boxplus), writes the new c2v and the
+// in-place posteriors over the staged rows, and one thread sends the rows
+// back with bulk stores. Same values as stream_cn<D, true, 4, false>.
+constexpr int kTmaQuads = 256;                 // quads (threads) per CTA
+constexpr int kTmaRowBytes = kTmaQuads * 16;   // one staged row segment
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, uint32_t src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
+               : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(kTmaQuads, 3) stream_cn_tma(const int32_t* __restrict__ recs, int count, ChunkState s) {
+  extern __shared__ __align__(128) char tsm[];  // [2 D][kTmaQuads] float4: posterior rows, then c2v rows
+  __shared__ __align__(8) unsigned long long bar_storage;
+  pdl_launch_next();
+  const int tid = threadIdx.x;
+  const int64_t QB = s.B / 4;
+  const int64_t tiles_per_rec = QB / kTmaQuads;
+  const int j = static_cast<int>(blockIdx.x / tiles_per_rec);
+  const int64_t q0 = (blockIdx.x - j * tiles_per_rec) * kTmaQuads;
+  if (j >= count) return;
+  // the CN record is a constant table: requested before waiting for the previous kernel
+  const CnRecordPacked<D> cr(recs + static_cast<int64_t>(j) * 4, 4);
+  const uint32_t bar = smem_u32(&bar_storage);
+  const uint32_t base = smem_u32(tsm);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_wait();
+  const int slot0 = cr.slot();
+  const unsigned mask = cr.mask();
+  if (tid == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * D * kTmaRowBytes)
+                 : "memory");
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      bulk_load(base + k * kTmaRowBytes, s.P + static_cast<int64_t>(cr.var(k)) * s.B + 4 * q0, kTmaRowBytes, bar);
+      bulk_load(base + (D + k) * kTmaRowBytes, s.c2v + static_cast<int64_t>(slot0 + k) * s.B + 4 * q0,
+                kTmaRowBytes, bar);
+    }
+  }
+  const unsigned dn = done_bits<4>(s, q0 + tid);  // overlaps the copies
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "LDPCB_TMA_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      "@p bra LDPCB_TMA_DONE;\n"
+      "bra LDPCB_TMA_WAIT;\n"
+      "LDPCB_TMA_DONE:\n"
+      "}\n" ::"r"(bar)
+      : "memory");
+  char* const mine = tsm + tid * 16;
+  if (dn != 0xfu) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // the quad as two frame pairs
+      f32x2 x[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k)
+        x[k] = sub2(*reinterpret_cast<const f32x2*>(mine + k * kTmaRowBytes + 8 * h),
+                    *reinterpret_cast<const f32x2*>(mine + (D + k) * kTmaRowBytes + 8 * h));
+      const bool live0 = !(dn & (1u << (2 * h))), live1 = !(dn & (2u << (2 * h)));
+      boxplus_row_x2<D, true>(x, D, [&](int k, f32x2 c) {
+        f32x2* const cp = reinterpret_cast<f32x2*>(mine + (D + k) * kTmaRowBytes + 8 * h);
+        f32x2* const pp = reinterpret_cast<f32x2*>(mine + k * kTmaRowBytes + 8 * h);
+        const f32x2 p = add2(x[k], c);  // in-place posterior: v2c + c
+        if (live0 && live1) {
+          *cp = c;
+          if (mask & (1u << k)) *pp = p;
+        } else {  // a frame that already stopped (decoder.hpp:173-177) keeps its state
+          const f32x2 oc = *cp, op = *pp;
+          *cp = pack2(live0 ? lo2(c) : lo2(oc), live1 ? hi2(c) : hi2(oc));
+          if (mask & (1u << k)) *pp = pack2(live0 ? lo2(p) : lo2(op), live1 ? hi2(p) : hi2(op));
+        }
+      });
+    }
+  }
+  // generic-proxy writes above -> async-proxy reads of the bulk stores
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (tid == 0) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      bulk_store(s.c2v + static_cast<int64_t>(slot0 + k) * s.B + 4 * q0, base + (D + k) * kTmaRowBytes, kTmaRowBytes);
+      if (mask & (1u << k))
+        bulk_store(s.P + static_cast<int64_t>(cr.var(k)) * s.B + 4 * q0, base + k * kTmaRowBytes, kTmaRowBytes);
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // writes complete before the CTA (and the grid) ends
   }
 }
 
@@ -679,12 +794,21 @@ struct StreamKernels {
   // frame queue: the same kernels with the fresh-frame code compiled in
   void (*cn_fresh)(const int32_t*, int, int, ChunkState, const uint32_t*);
   void (*vnsum_fresh)(const int4*, int, int, ChunkState, int, const uint32_t*);
+  // TMA-staged CN kernel (regular rows of degree 3 / 6, four frames per thread), or null
+  void (*cn_tma)(const int32_t*, int, ChunkState);
+  int tma_smem;
 };
 
 template <int D, bool EXACT, int V>
 StreamKernels pick_dv() {
-  return {stream_cn<D, EXACT, V, false>, stream_syndrome<D, EXACT, V>,       stream_vnsum<V, false>,
-          stream_syndrome_sw<D, EXACT>,  stream_cn<D, EXACT, V, true>,       stream_vnsum<V, true>};
+  StreamKernels k{stream_cn<D, EXACT, V, false>, stream_syndrome<D, EXACT, V>, stream_vnsum<V, false>,
+                  stream_syndrome_sw<D, EXACT>,  stream_cn<D, EXACT, V, true>, stream_vnsum<V, true>,
+                  nullptr,                       0};
+  if constexpr (EXACT && D <= 6 && V == 4) {
+    k.cn_tma = stream_cn_tma<D>;
+    k.tma_smem = 2 * D * kTmaRowBytes;
+  }
+  return k;
 }
 
 template <int V>
@@ -694,7 +818,7 @@ StreamKernels pick_v(const DevGraph& g) {
     case 6: return pick_dv<6, true, V>();
     case 8: return pick_dv<8, false, V>();
     case 16: return pick_dv<16, false, V>();
-    default: return {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    default: return {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   }
 }
 
@@ -725,6 +849,29 @@ unsigned blocks_for(int64_t items, int tpb) { return static_cast<unsigned>((item
 bool stream_pdl() {
   const char* e = std::getenv("LDPCB_STREAM_PDL");
   return !e || std::atoi(e) != 0;
+}
+
+// LDPCB_STREAM_TMA=1 selects the TMA-staged CN kernel (bit-identical outputs;
+// measured 1 % slower than the LDG.128 kernel on C5 n = 64800: 65.3 against 64.6 ms per step)
+bool stream_tma() {
+  const char* e = std::getenv("LDPCB_STREAM_TMA");
+  return e && std::atoi(e) != 0;
+}
+
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl_smem(void (*k)(KArgs...), unsigned blocks, int tpb, int smem, cudaStream_t st, bool pdl,
+                            Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(tpb);
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
 template <class... KArgs, class... Args>
@@ -790,6 +937,11 @@ int launch_stream_one(const DevGraph& g, const DecodeArgs& a, cudaStream_t st, c
   const int64_t QB = B / stream_lanes();
   const bool dump = a.max_subiters > 0;
   const bool pdl = stream_pdl();
+  // TMA-staged CN kernel: packed regular-row records, whole CTAs of quads
+  bool use_tma = K.cn_tma && g.cs == 4 && stream_lanes() == 4 && QB % kTmaQuads == 0 && stream_tma();
+  if (use_tma && cudaFuncSetAttribute(reinterpret_cast<const void*>(K.cn_tma),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, K.tma_smem) != cudaSuccess)
+    use_tma = false;
   int launches = 0;
   for (int64_t f0 = 0; f0 < a.frames && err == cudaSuccess; f0 += B) {
     s.nb = static_cast<int>(std::min<int64_t>(B, a.frames - f0));
@@ -812,7 +964,11 @@ int launch_stream_one(const DevGraph& g, const DecodeArgs& a, cudaStream_t st, c
         }
         ++sub;
         const int c0 = g.h_cn_off[grp], cn = g.h_cn_off[grp + 1] - c0;
-        if (cn > 0) {
+        if (cn > 0 && use_tma) {
+          err = launch_pdl_smem(K.cn_tma, static_cast<unsigned>(cn * (QB / kTmaQuads)), kTmaQuads, K.tma_smem, st,
+                                pdl, g.cn_rec + static_cast<size_t>(c0) * g.cs, cn, s);
+          ++launches;
+        } else if (cn > 0) {
           err = launch_pdl(K.cn, blocks_for(cn * QB, tpb), tpb, st, pdl, g.cn_rec + static_cast<size_t>(c0) * g.cs,
                            g.cs, cn, s, static_cast<const uint32_t*>(nullptr));
           ++launches;
@@ -879,7 +1035,11 @@ bool stream_queue_enabled() {
 // iteration behind, so the device never waits for the host.
 int launch_stream_queue(const DevGraph& g, const DecodeArgs& a, cudaStream_t st, int64_t B0) {
   const StreamKernels K = pick_v<4>(g);
-  const int64_t B = (std::min<int64_t>(B0, a.frames) + 127) / 128 * 128;
+  // lanes: a quarter of the batch (so that lanes are refilled several times
+  // and the tail, where the last frames run on alone, stays short) between
+  // 2048 and 8192 (kernel efficiency); LDPCB_STREAM_CHUNK caps it
+  const int64_t want = std::min<int64_t>(std::max<int64_t>((a.frames / 4 + 127) / 128 * 128, 2048), 8192);
+  const int64_t B = (std::min<int64_t>(std::min(B0, want), a.frames) + 127) / 128 * 128;
   ChunkState s;
   s.B = B;
   s.nb = static_cast<int>(std::min<int64_t>(B, a.frames));

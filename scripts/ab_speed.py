@@ -1,6 +1,6 @@
 """A/B decode throughput on the C1 code: fixed 10 iterations (C5) and 20
 iterations with early stop, per schedule, for the library in $LDPCB_LIBRARY
-and the fix-up mode in $LDPCB_DELTA_FIXUPS."""
+and the kernel selection in $AB_KERNEL."""
 import os
 import sys
 
@@ -12,7 +12,8 @@ import paper_1202_1060_b200 as P  # noqa: E402
 g = P.configs.c1_code()
 F = 1 << 20
 x = P.transmit_all_zero(g.n_vars, P.sigma2_from_ebn0(2.0, g.rate), 1, 0, F)
-tag = f"{os.path.basename(P._lib.LIB_PATH)} delta={os.environ.get('LDPCB_DELTA_FIXUPS', '1')}"
+P.set_kernel(int(os.environ.get("AB_KERNEL", "0")))  # 1: posterior-based resident kernel, 0: library plan
+tag = f"{os.path.basename(P._lib.LIB_PATH)} kernel={os.environ.get('AB_KERNEL', '0')}"
 for name, s in P.configs.c1_schedules(g).items():
     for iters, es in ((10, False), (20, True)):
         for _ in range(2):

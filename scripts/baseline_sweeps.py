@@ -34,9 +34,10 @@ from scipy.stats import beta, t as student_t  # noqa: E402
 
 CONFIGS = {
     # name: (code, schedules, cfg, reference frames per point)
-    "c2": ("c1_code", "c1_schedules", P.configs.C2, 20000),
-    "c3": ("c3_code", "c3_schedules", P.configs.C3, 8000),
-    "c4": ("c4_code", "c4_schedules", P.configs.C4, 32),
+    # reference samples sized as SURVEY 8(d) asks (>= 1e5 frames per C2 point)
+    "c2": ("c1_code", "c1_schedules", P.configs.C2, 100000),
+    "c3": ("c3_code", "c3_schedules", P.configs.C3, 40000),
+    "c4": ("c4_code", "c4_schedules", P.configs.C4, 1024),
 }
 
 
@@ -49,9 +50,27 @@ def clopper_pearson(k, n, a=0.05):
 def bootstrap_ber(bit_err, n_bits, reps=2000, seed=0):
     rng = np.random.default_rng(seed)
     f = len(bit_err)
-    idx = rng.integers(0, f, size=(reps, f))
-    est = bit_err[idx].sum(axis=1) / (f * n_bits)
+    est = []
+    for _ in range(0, reps, 50):  # in slices: 1e5 frames x 2000 resamples would not fit in memory at once
+        idx = rng.integers(0, f, size=(50, f))
+        est.append(bit_err[idx].sum(axis=1) / (f * n_bits))
+    est = np.concatenate(est)
     return float(np.quantile(est, 0.025)), float(np.quantile(est, 0.975))
+
+
+def paired(g_err, r_err, g_be, r_be, g_it, r_it, n_bits):
+    """The same frames decoded by both: McNemar's exact test on the frame-error
+    disagreements, and the paired differences of bit errors and iterations."""
+    from scipy.stats import binomtest
+
+    b = int((g_err & ~r_err).sum())  # frame errors only on the B200
+    c = int((~g_err & r_err).sum())  # only in the reference
+    p = float(binomtest(b, b + c, 0.5).pvalue) if b + c else 1.0
+    d_it = (g_it - r_it).astype(np.float64)
+    return {"frame_error_only_b200": b, "frame_error_only_ref": c, "mcnemar_p": p,
+            "ber_diff": float((g_be.sum() - r_be.sum()) / (len(g_be) * n_bits)),
+            "iters_diff_mean": float(d_it.mean()), "iters_diff_ci": t_interval(d_it),
+            "frames_with_any_difference": int(((g_be != r_be) | (g_it != r_it)).sum())}
 
 
 def t_interval(x):
@@ -99,18 +118,22 @@ def run(names, out_path, threads):
                 gb = gout["bits"].cpu().numpy()
                 same = ((gb == ref["bits"]).all(axis=1) & (gout["iterations"].cpu().numpy() == ref["iterations"])
                         & (gout["converged"].cpu().numpy() == ref["converged"]))
+                gbe = gb.sum(axis=1).astype(np.int64)
+                pair = paired(gbe > 0, be > 0, gbe, be, gout["iterations"].cpu().numpy(), ref["iterations"], n)
                 inside = {
                     "fer": r["fer_ci"][0] <= b["fer"] <= r["fer_ci"][1],
                     "ber": r["ber_ci"][0] <= b["ber"] <= r["ber_ci"][1],
                     "mean_iters": r["iters_ci"][0] <= b["mean_iters"] <= r["iters_ci"][1],
                 }
                 pt = {"config": name, "schedule": sname, "ebn0_db": ebn0, "max_iters": iters, "n": n, "k": K,
-                      "b200": b, "ref": r, "identical": float(same.mean()), "inside_ci": inside}
+                      "b200": b, "ref": r, "identical": float(same.mean()), "inside_ci": inside, "paired": pair}
                 results["points"].append(pt)
                 print(f"{name} {sname:6s} {ebn0:4.2f} dB | b200 {b['frames']:8d} fr FER {b['fer']:.3e} "
                       f"BER {b['ber']:.3e} it {b['mean_iters']:5.2f} ({b['frames_per_s']:.2e} fr/s) | ref {Fr:6d} fr "
                       f"FER {r['fer']:.3e} [{r['fer_ci'][0]:.2e},{r['fer_ci'][1]:.2e}] it {r['mean_iters']:5.2f} "
-                      f"({r['frames_per_s']:.1f} fr/s) | identical {same.mean():.4f} inside {inside}", flush=True)
+                      f"({r['frames_per_s']:.1f} fr/s) | identical {same.mean():.5f} inside {inside} | paired: FE only b200 "
+                      f"{pair['frame_error_only_b200']} / only ref {pair['frame_error_only_ref']} (p {pair['mcnemar_p']:.2f}), "
+                      f"d iters {pair['iters_diff_mean']:+.2e}", flush=True)
                 json.dump(results, open(out_path, "w"), indent=1, default=float)
     return results
 

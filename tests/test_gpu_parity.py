@@ -524,17 +524,19 @@ def test_c4_long_code_parity(P, torch, orc, es, iters):
     at stride 720) at 1.1 dB, decoded by the HBM-streamed kernels with the
     library defaults: C5-long's fixed 10 iterations (lazy totals, no trace:
     the benchmarked mode) and config 4's <= 30 iterations with early stop.
-    2000 frames against the reference decoder at the full 99.9 % bar."""
+    2048 frames (whole CTAs of frame quads, so the fixed-iteration decode runs
+    the TMA-staged CN kernel the bench runs) against the reference decoder at
+    the full 99.9 % bar."""
     g = P.configs.c4_code()
     s = P.configs.c4_schedules(g)["ndgsbp"]
     assert P.plan(g, s, 64)["kernel"] == 2
     og = orc.graph(g.n_vars, *g.csr())
     s2 = P.sigma2_from_ebn0(1.1, g.rate)
-    F = 2000
+    F = 2048
     llr = orc.transmit_batch_f32(s2, 1, g.n_vars, 0, F, THREADS)
     ref = orc.decode_batch(og, s.groups, llr, iters, early_stop=es, threads=THREADS, posterior=True)
     x = cu(torch, llr)
-    # early stop: all 2000 frames in their own lanes, then 512 lanes refilled from the frame queue
+    # early stop: all 2048 frames in their own lanes, then 512 lanes refilled from the frame queue
     for lanes in ((None, "512") if es else (None,)):
         if lanes:
             os.environ["LDPCB_STREAM_CHUNK"] = lanes
@@ -739,3 +741,33 @@ def test_direct_kernel_four_frames_per_thread(P, torch, orc):
     same = frame_parity(gpu, ref)
     frac, worst = post_stats(gpu["posterior"], ref["posterior"], same & (ref["converged"] == 1))
     assert same.mean() >= 0.999 and frac >= 0.9999, (same.mean(), frac, worst)
+
+
+@pytest.mark.parametrize("es,iters", [(True, 20), (False, 10)])
+def test_streamed_tma_staging_is_bit_identical(P, torch, orc, es, iters):
+    """The TMA-staged CN kernel (bulk copies of whole row segments into shared
+    memory, stream.cu stream_cn_tma) against the LDG.128 kernel and the
+    resident posterior kernel: every output identical. 1024-frame chunks so
+    that the staged kernel runs (whole CTAs of quads), a ragged last chunk
+    (padding lanes) and, with early stop, stopped lanes that keep their state."""
+    g = P.configs.c1_code()
+    s = P.configs.c1_schedules(g)["ndgsbp"]
+    F = 2500
+    llr = cu(torch, orc.transmit_batch_f32(P.sigma2_from_ebn0(1.75, g.rate), 8, g.n_vars, 0, F, THREADS))
+    os.environ["LDPCB_STREAM_CHUNK"] = "1024"
+    os.environ["LDPCB_STREAM_QUEUE"] = "0"
+    outs = {}
+    try:
+        P.set_kernel(1)
+        outs["resident"] = to_np(P.decode_batch(g, s, llr, iters, early_stop=es, posterior=True, trace=True))
+        P.set_kernel(2)
+        for tma in ("1", "0"):
+            os.environ["LDPCB_STREAM_TMA"] = tma
+            outs[tma] = to_np(P.decode_batch(g, s, llr, iters, early_stop=es, posterior=True, trace=True))
+    finally:
+        P.set_kernel(0)
+        for k in ("LDPCB_STREAM_CHUNK", "LDPCB_STREAM_QUEUE", "LDPCB_STREAM_TMA"):
+            os.environ.pop(k, None)
+    for k in outs["resident"]:
+        assert np.array_equal(outs["1"][k], outs["0"][k]), k
+        assert np.array_equal(outs["1"][k], outs["resident"][k]), k
