@@ -49,7 +49,7 @@ MUFU_PER_EDGE = 3  # SASS-counted: 1 MUFU.EX2 + 2 MUFU.LG2 per CN-edge update (d
 MUFU_PER_SM_CLK = 16
 HBM_BYTES_PER_EDGE = 8  # streamed decoder: c2v read + write per CN-edge update (fp32)
 HBM_BYTES_PER_TOUCH = 8  # posterior read + write per distinct VN a group touches (fp32)
-DEFAULT_FRAMES = {"c5_n1008": 1 << 21, "c5_n64800": 8192}
+DEFAULT_FRAMES = {"c5_n1008": 1 << 21, "c5_n64800": 32768}
 FIXTURE = os.path.join(ROOT, "bench_fixtures", "c5_workloads.npz")
 DESC = {
     "c5_n1008": "C5: (3,6)-regular n=1008 girth>=6 (seed 1), NDGSBP 8 windows x 84 CNs stride 63, Eb/N0 2.0 dB",

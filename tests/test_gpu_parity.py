@@ -524,9 +524,7 @@ def test_c4_long_code_parity(P, torch, orc, es, iters):
     at stride 720) at 1.1 dB, decoded by the HBM-streamed kernels with the
     library defaults: C5-long's fixed 10 iterations (lazy totals, no trace:
     the benchmarked mode) and config 4's <= 30 iterations with early stop.
-    2048 frames (whole CTAs of frame quads, so the fixed-iteration decode runs
-    the TMA-staged CN kernel the bench runs) against the reference decoder at
-    the full 99.9 % bar."""
+    2048 frames against the reference decoder at the full 99.9 % bar."""
     g = P.configs.c4_code()
     s = P.configs.c4_schedules(g)["ndgsbp"]
     assert P.plan(g, s, 64)["kernel"] == 2
