@@ -681,10 +681,14 @@ int ldpcb_decode_host(ldpcb_code code, ldpcb_schedule s, int64_t frames, const f
         cuda_check(cudaMemsetAsync(buf[k].cnt, 0, 6 * sizeof(int64_t), st[k]), "cudaMemsetAsync");
       }
     }
+    // Streamed decodes: a call takes (first chunk's copy) + (all decodes), the later copies
+    // hide behind decodes. A quarter-size first chunk starts the device four times sooner
+    // (C5 n = 64800, 32768 frames: 38 ms of exposed copy become 10).
+    const int64_t first = (p0.kernel == 2 && frames > chunk) ? std::max<int64_t>(1024, chunk / 4 / 4 * 4) : chunk;
     int64_t slot = 0;
-    for (int64_t c0 = 0; c0 < frames; c0 += chunk, ++slot) {
+    for (int64_t c0 = 0, cnt = 0; c0 < frames; c0 += cnt, ++slot) {
       const int k = static_cast<int>(slot % kSlots);
-      const int64_t cnt = std::min(chunk, frames - c0);
+      cnt = std::min(slot == 0 ? std::min(first, chunk) : chunk, frames - c0);
       cuda_check(cudaMemcpyAsync(buf[k].llr, llr + c0 * n, cnt * n * sizeof(float), cudaMemcpyHostToDevice, st[k]),
                  "H2D");
       ldpcb::DecodeArgs a;
