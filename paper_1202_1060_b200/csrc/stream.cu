@@ -48,6 +48,7 @@ struct ChunkState {
   // frame queue (launch_stream_queue)
   int64_t* frame = nullptr;           // [B] frame id held by each lane, -1 idle
   unsigned* sw = nullptr;             // [n][B/32] hard-decision sign words
+  unsigned* fail = nullptr;           // [B/32] lanes failing some parity check (no-trace syndrome test), or null
   int* list = nullptr;                // [B] lanes retiring this iteration
   int* ctl = nullptr;                 // [0] retiring lanes, [1] lanes decoding
   unsigned long long* next = nullptr; // next frame id to hand out
@@ -594,57 +595,105 @@ __device__ __forceinline__ float exact_posterior(const ChunkState& s, const int4
 
 // Hard-decision sign words: sw[p][B/32], word 4W + i bit b = sign of lane
 // 4 (32 W + b) + i, one warp per (VN position, 128 lanes). B % 128 == 0.
+constexpr int kSignRows = 4;  // VN positions per thread: their posterior loads are in flight together
 __global__ void __launch_bounds__(256) stream_signs(const int4* __restrict__ all_vn, int vs4, int n, ChunkState s) {
   pdl_launch_next();
   const int64_t QB = s.B / 4;
   const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int blocks = (n + kSignRows - 1) / kSignRows;
   pdl_wait();
-  if (item >= n * QB) return;  // whole warps (n * QB is a multiple of 32)
-  const int p = static_cast<int>(item / QB);
-  const int64_t q = item - p * QB;
+  // the parity-failure words of this iteration's syndrome test start empty (stream_syndrome_or)
+  if (s.fail && item < s.B / 32) s.fail[item] = 0u;
+  if (item >= blocks * QB) return;  // whole warps (QB is a multiple of 32)
+  const int p0 = static_cast<int>(item / QB) * kSignRows;
+  const int64_t q = item - (p0 / kSignRows) * QB;
   const States<4> st = load_states<4>(s, q);
   const unsigned dn = done_bits<4>(st);
-  Vec<4> x;
-  if (dn != 0xfu) x = ldv<4>(s.P + static_cast<int64_t>(p) * s.B + 4 * q);
-  unsigned neg = 0;
-  bool near = false;
+  Vec<4> xs[kSignRows];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) near |= !(dn & (1u << i)) && fabsf(x.v[i]) < kNearZero;
-  if (near) {  // rare: the exact totals of the quad (16-byte loads, as stream_vnsum)
-    const int4* rec = all_vn + static_cast<int64_t>(p) * vs4;
-    int4 t = __ldg(rec);
-    Vec<4> acc = ldv<4>(s.L + static_cast<int64_t>(t.x) * s.B + 4 * q);
-    const int zero = s.zero_slot;
-    auto add = [&](int slot) {
-      if (slot == zero) return;
-      const Vec<4> c = ldv<4>(s.c2v + static_cast<int64_t>(slot) * s.B + 4 * q);
+  for (int r = 0; r < kSignRows; ++r)
+    if (dn != 0xfu && p0 + r < n) xs[r] = ldv<4>(s.P + static_cast<int64_t>(p0 + r) * s.B + 4 * q);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) acc.v[i] += c.v[i];
-    };
-    add(t.y);
-    add(t.z);
-    add(t.w);
-    for (int r = 1; r < vs4 && t.w != zero; ++r) {
-      t = __ldg(rec + r);
-      add(t.x);
+  for (int r = 0; r < kSignRows; ++r) {
+    const int p = p0 + r;
+    if (p >= n) break;  // warp-uniform
+    Vec<4>& x = xs[r];
+    unsigned neg = 0;
+    bool near = false;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) near |= !(dn & (1u << i)) && fabsf(x.v[i]) < kNearZero;
+    if (near) {  // rare: the exact totals of the quad (16-byte loads, as stream_vnsum)
+      const int4* rec = all_vn + static_cast<int64_t>(p) * vs4;
+      int4 t = __ldg(rec);
+      Vec<4> acc = ldv<4>(s.L + static_cast<int64_t>(t.x) * s.B + 4 * q);
+      const int zero = s.zero_slot;
+      auto add = [&](int slot) {
+        if (slot == zero) return;
+        const Vec<4> c = ldv<4>(s.c2v + static_cast<int64_t>(slot) * s.B + 4 * q);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc.v[i] += c.v[i];
+      };
       add(t.y);
       add(t.z);
       add(t.w);
+      for (int rr = 1; rr < vs4 && t.w != zero; ++rr) {
+        t = __ldg(rec + rr);
+        add(t.x);
+        add(t.y);
+        add(t.z);
+        add(t.w);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (fabsf(x.v[i]) < kNearZero) x.v[i] = acc.v[i];
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      if (fabsf(x.v[i]) < kNearZero) x.v[i] = acc.v[i];
+      if (!(dn & (1u << i))) neg |= static_cast<unsigned>(x.v[i] < 0.f) << i;  // tie -> 0 (decoder.hpp:166)
+    uint4 w;
+    w.x = __ballot_sync(0xffffffffu, neg & 1u);
+    w.y = __ballot_sync(0xffffffffu, neg & 2u);
+    w.z = __ballot_sync(0xffffffffu, neg & 4u);
+    w.w = __ballot_sync(0xffffffffu, neg & 8u);
+    if ((threadIdx.x & 31) == 0)
+      *reinterpret_cast<uint4*>(s.sw + static_cast<int64_t>(p) * (s.B / 32) + 4 * (q / 32)) = w;
   }
+}
+
+// Which lanes fail some parity check (decoder.hpp:129-137, 173): all an early
+// stop without a trace needs. One thread per (32 CNs, 128 lanes): the CN's
+// parity over 128 lanes is the XOR of its VNs' sign words (one uint4 each),
+// ORed over the thread's CNs and then into fail[] (cleared by stream_signs).
+// stream_q_iter_end reads a lane's bit as its syndrome weight (0 / 1).
+constexpr int kOrRows = 32;
+template <int D, bool EXACT>
+__global__ void __launch_bounds__(256) stream_syndrome_or(const int32_t* __restrict__ recs, int CS, int m,
+                                                          ChunkState s) {
+  pdl_launch_next();
+  const int cols = static_cast<int>(s.B / 128);  // uint4 columns of the sign words
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int blk = static_cast<int>(item / cols), col = static_cast<int>(item - static_cast<int64_t>(blk) * cols);
+  pdl_wait();
+  if (item == 0) s.ctl[0] = 0;  // the retire list of this iteration starts empty
+  if (blk * kOrRows >= m) return;
+  uint4 acc = make_uint4(0u, 0u, 0u, 0u);
+  const int r1 = min(m, (blk + 1) * kOrRows);
+  for (int r = blk * kOrRows; r < r1; ++r) {
+    const CnRecord<D, EXACT> cr(recs + static_cast<int64_t>(r) * CS, CS);
+    uint4 par = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-    if (!(dn & (1u << i))) neg |= static_cast<unsigned>(x.v[i] < 0.f) << i;  // tie -> 0 (decoder.hpp:166)
-  uint4 w;
-  w.x = __ballot_sync(0xffffffffu, neg & 1u);
-  w.y = __ballot_sync(0xffffffffu, neg & 2u);
-  w.z = __ballot_sync(0xffffffffu, neg & 4u);
-  w.w = __ballot_sync(0xffffffffu, neg & 8u);
-  if ((threadIdx.x & 31) == 0)
-    *reinterpret_cast<uint4*>(s.sw + static_cast<int64_t>(p) * (s.B / 32) + 4 * (q / 32)) = w;
+    for (int k = 0; k < D; ++k) {
+      if (!cr.has(k)) continue;
+      const uint4 w = __ldcg(reinterpret_cast<const uint4*>(s.sw + static_cast<int64_t>(cr.var(k)) * (s.B / 32)) + col);
+      par.x ^= w.x, par.y ^= w.y, par.z ^= w.z, par.w ^= w.w;
+    }
+    acc.x |= par.x, acc.y |= par.y, acc.z |= par.z, acc.w |= par.w;
+  }
+  unsigned* f = s.fail + 4 * col;
+  if (acc.x) atomicOr(f, acc.x);
+  if (acc.y) atomicOr(f + 1, acc.y);
+  if (acc.z) atomicOr(f + 2, acc.z);
+  if (acc.w) atomicOr(f + 3, acc.w);
 }
 
 // Syndrome weight per lane (decoder.hpp:129-137) from the sign words.
@@ -691,7 +740,8 @@ __global__ void stream_q_iter_end(ChunkState s, int early_stop, int32_t* trace, 
   pdl_enter();
   const int64_t f = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (f >= s.B || (s.done[f] & 1)) return;
-  const int w = s.weight[f];
+  // lane f = 4 (32 W + b) + i is bit b of word 4 W + i (the sign-word layout)
+  const int w = s.fail ? static_cast<int>((s.fail[4 * (f / 128) + (f & 3)] >> ((f >> 2) & 31)) & 1u) : s.weight[f];
   s.weight[f] = 0;
   const int it = ++s.iters[f];
   if (trace) trace[s.frame[f] * max_iters + it - 1] = w;
@@ -797,13 +847,15 @@ struct StreamKernels {
   // TMA-staged CN kernel (regular rows of degree 3 / 6, four frames per thread), or null
   void (*cn_tma)(const int32_t*, int, ChunkState);
   int tma_smem;
+  void (*syn_or)(const int32_t*, int, int, ChunkState);  // frame queue without a trace
 };
 
 template <int D, bool EXACT, int V>
 StreamKernels pick_dv() {
   StreamKernels k{stream_cn<D, EXACT, V, false>, stream_syndrome<D, EXACT, V>, stream_vnsum<V, false>,
                   stream_syndrome_sw<D, EXACT>,  stream_cn<D, EXACT, V, true>, stream_vnsum<V, true>,
-                  nullptr,                       0};
+                  nullptr,                       0,
+                  stream_syndrome_or<D, EXACT>};
   if constexpr (EXACT && D <= 6 && V == 4) {
     k.cn_tma = stream_cn_tma<D>;
     k.tma_smem = 2 * D * kTmaRowBytes;
@@ -818,7 +870,7 @@ StreamKernels pick_v(const DevGraph& g) {
     case 6: return pick_dv<6, true, V>();
     case 8: return pick_dv<8, false, V>();
     case 16: return pick_dv<16, false, V>();
-    default: return {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
+    default: return {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr};
   }
 }
 
@@ -1048,7 +1100,7 @@ int launch_stream_queue(const DevGraph& g, const DecodeArgs& a, cudaStream_t st,
   const size_t lanes = 5 * 4 * B + 8 * B + 4 * B + 64;
   const size_t signs = 4ull * g.n * (B / 32);
   char* mem = nullptr;
-  cudaError_t err = cudaMallocAsync(reinterpret_cast<void**>(&mem), state + lanes + signs, st);
+  cudaError_t err = cudaMallocAsync(reinterpret_cast<void**>(&mem), state + lanes + signs + 4 * (B / 32) + 16, st);
   if (err != cudaSuccess) return static_cast<int>(err);
   s.c2v = reinterpret_cast<float*>(mem);
   s.P = s.c2v + static_cast<size_t>(g.n_slots) * B;
@@ -1063,6 +1115,8 @@ int launch_stream_queue(const DevGraph& g, const DecodeArgs& a, cudaStream_t st,
   s.ctl = s.list + B;
   s.next = reinterpret_cast<unsigned long long*>(s.ctl + 8);
   s.sw = reinterpret_cast<unsigned*>(mem + state + lanes);
+  // without a trace only "does any check fail" is needed per lane (stream_syndrome_or)
+  if (!a.trace && K.syn_or) s.fail = reinterpret_cast<unsigned*>(mem + state + lanes + signs);
   // the host's view of the decoding-lane count, one slot per parity of the iteration
   thread_local int* host_live = nullptr;
   if (!host_live && cudaMallocHost(reinterpret_cast<void**>(&host_live), 2 * sizeof(int)) != cudaSuccess) {
@@ -1109,9 +1163,12 @@ int launch_stream_queue(const DevGraph& g, const DecodeArgs& a, cudaStream_t st,
       }
     }
     if (err != cudaSuccess) break;
-    err = launch_pdl(stream_signs, blocks_for(g.n * QB, tpb), tpb, st, pdl,
+    err = launch_pdl(stream_signs, blocks_for((g.n + kSignRows - 1) / kSignRows * QB, tpb), tpb, st, pdl,
                      reinterpret_cast<const int4*>(g.all_vn_rec), g.vs4, g.n, s);
-    if (err == cudaSuccess)
+    if (err == cudaSuccess && s.fail)
+      err = launch_pdl(K.syn_or, blocks_for(static_cast<int64_t>((g.m + kOrRows - 1) / kOrRows) * (B / 128), tpb), tpb,
+                       st, pdl, g.all_rec, g.cs, g.m, s);
+    else if (err == cudaSuccess)
       err = launch_pdl(K.syn_sw, blocks_for(g.m * QB, tpb), tpb, st, pdl, g.all_rec, g.cs, g.m, s);
     if (err == cudaSuccess)
       err = launch_pdl(stream_q_iter_end, blocks_for(B, tpb), tpb, st, pdl, s, a.early_stop, a.trace, a.max_iters);
