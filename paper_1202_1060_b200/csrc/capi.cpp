@@ -305,6 +305,7 @@ ldpcb::DevGraph dev_graph(ldpcb_code code, ldpcb_schedule s) {
     g.d_fv = dt.fv;
     g.d_cells = dt.cells;
     g.d_l_base = dt.l_base;
+    g.d_buf_cells = dt.buf_cells;
     g.d_max_items = dt.max_items;
     for (size_t i = 0; i < dt.cn_off.size(); ++i) g.d_goff[i] = static_cast<uint16_t>(dt.cn_off[i]);
     g.d_cn_rec = d.d_cn_rec;

@@ -52,6 +52,8 @@ namespace {
 using namespace dev;
 
 constexpr int kDirectThreads = 96;  // C1 NDGSBP: 84 CN items per group
+constexpr int kFloodThreads = 256;  // flooding: 504 CN items per iteration in two rounds; two CTAs per SM at 128 registers
+                                    // (18 warps per SM would cap the kernel at 96 registers: 88 bytes of spills)
 
 // The CTA's dynamic shared memory: the cell array, then the hard-decision
 // bytes. Every device function addresses it
@@ -195,6 +197,48 @@ __device__ __forceinline__ void direct_group(const DevGraph& g, int tid, int grp
   cn = ncn;
 }
 
+// One flooding iteration (a single group of more CNs than threads): every
+// thread runs its CN items round after round, reading the edge cells at byte
+// offset rd and writing those at wr (the two copies, swapped by the caller
+// every iteration), so no item can read a message of this iteration and no
+// barrier is needed inside the iteration (Jacobi, decoder.hpp:107-113).
+template <int FV>
+__device__ __forceinline__ void direct_flood_iteration(const DevGraph& g, int tid, int nt, uint32_t rd, uint32_t wr) {
+  const int cn = g.d_goff[1] - g.d_goff[0];
+  DRec next_rec;
+  if (tid < cn) next_rec.load(g.d_cn_rec + static_cast<size_t>(tid) * 12);
+  for (int j = tid; j < cn; j += nt) {
+    const DRec cur = next_rec;
+    if (j + nt < cn) next_rec.load(g.d_cn_rec + static_cast<size_t>(j + nt) * 12);
+    const int w[10] = {cur.a.x, cur.a.y, cur.a.z, cur.a.w, cur.b.x, cur.b.y, cur.b.z, cur.b.w, cur.c.x, cur.c.y};
+    Cell<FV> x[6], lh[2];
+    uint32_t own[6];
+    const char* const src = dsm + rd;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      own[k] = lo16(w[2 * k]);
+      const Cell<FV> cx = ld_cell<FV>(src, hi16(w[2 * k]));
+      const Cell<FV> cy = ld_cell<FV>(src, lo16(w[2 * k + 1]));
+      lh[k] = ld_cell<FV>(dsm, hi16(w[2 * k + 1]));
+      x[k] = add_cell<FV>(add_cell<FV>(cx, cy), lh[k]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      auto field = [&](int i) { return (i & 1) ? hi16(w[4 + i / 2]) : lo16(w[4 + i / 2]); };
+      own[2 + q] = field(3 * q);
+      x[2 + q] = add_cell<FV>(ld_cell<FV>(src, field(3 * q + 1)), ld_cell<FV>(src, field(3 * q + 2)));
+    }
+    static_assert(FV == 2, "flooding runs two frames per thread");
+    f32x2 xi[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) xi[k] = x[k].p[0];
+    boxplus_row_x2<6, true>(xi, 6, [&](int k, f32x2 c) {
+      *reinterpret_cast<f32x2*>(dsm + wr + own[k]) = k < 2 ? add2(c, lh[k].p[0]) : c;
+    });
+    next_rec.pin();
+  }
+}
+
 // Per-CTA control state (shared memory): slot ff holds frame `frame[ff]`
 // (-1: none); done: 0 decoding, 1 idle, 2 retiring, 3 refilled this round.
 template <int FV>
@@ -215,7 +259,7 @@ __device__ __forceinline__ long long direct_pull(unsigned long long* queue, int6
 // and the holder cells (0 + L). All global loads of a batch of elements are
 // issued before any is used. The iteration-boundary functions are kept out
 // of line: the sub-iteration loop then owns the whole register budget.
-template <int FV>
+template <int FV, bool FLOOD>
 __device__ __forceinline__ void direct_load_slots(const DevGraph& g, const DecodeArgs& a, const DirectCtl<FV>* ctl,
                                                   unsigned mask) {
   constexpr int CB = 4 * FV;
@@ -244,6 +288,8 @@ __device__ __forceinline__ void direct_load_slots(const DevGraph& g, const Decod
       const float y = f >= 0 ? clamp_llr(raw) * kLog2e : kClampB;
       *reinterpret_cast<float*>(sb + l_off + pos * CB) = y;
       *reinterpret_cast<float*>(sb + hold) = y;
+      if constexpr (FLOOD)  // both copies of the edge cells
+        *reinterpret_cast<float*>(sb + hold + static_cast<uint32_t>(g.d_buf_cells) * CB) = y;
     };
     if (f >= 0 && vec) {
       const float4* l4 = reinterpret_cast<const float4*>(a.llr + f * n);
@@ -282,9 +328,11 @@ __device__ __forceinline__ void direct_load_slots(const DevGraph& g, const Decod
 // it_cta: iterations since the CTA's slots were last refilled together (fixed
 // iteration counts). Returns 0: carry on, 1: slots were refilled, 2: no slot
 // is busy and the queue is empty.
-template <int FV>
+template <int FV, bool FLOOD>
 __device__ __forceinline__ int direct_iteration_end(const DevGraph& g, const DecodeArgs& a,
-                                                    unsigned long long* queue, DirectCtl<FV>* ctl, int it_cta) {
+                                                    unsigned long long* queue, DirectCtl<FV>* ctl, int it_cta,
+                                                    uint32_t rd_flood) {  // byte offset of the current edge cells
+  const uint32_t rd = FLOOD ? rd_flood : 0u;
   constexpr int CB = 4 * FV;
   const int tid = threadIdx.x, nt = blockDim.x, n = g.n, m = g.m;
   uint8_t* const s_hd = reinterpret_cast<uint8_t*>(dsm + static_cast<size_t>(g.d_cells) * CB);  // [n] bit i = frame i
@@ -293,8 +341,8 @@ __device__ __forceinline__ int direct_iteration_end(const DevGraph& g, const Dec
   // hard decisions (tie -> 0) from the totals ((c2v_h + L) + c2v) + c2v, one sign bit per frame
   for (int pos = tid; pos < n; pos += nt) {
     const int2 r = __ldg(reinterpret_cast<const int2*>(g.d_vn_rec) + pos);
-    Cell<FV> t = add_cell<FV>(ld_cell<FV>(dsm, lo16(r.x)), ld_cell<FV>(dsm, hi16(r.x)));
-    t = add_cell<FV>(t, ld_cell<FV>(dsm, lo16(r.y)));
+    Cell<FV> t = add_cell<FV>(ld_cell<FV>(dsm + rd, lo16(r.x)), ld_cell<FV>(dsm + rd, hi16(r.x)));
+    t = add_cell<FV>(t, ld_cell<FV>(dsm + rd, lo16(r.y)));
     s_hd[pos] = static_cast<uint8_t>(sign_bits<FV>(t));
   }
   __syncthreads();
@@ -357,7 +405,7 @@ __device__ __forceinline__ int direct_iteration_end(const DevGraph& g, const Dec
     }
     if (errs) atomicAdd(&ctl->berr[ff], errs);
     if (a.posterior) {
-      const char* const sb = dsm + 4 * ff;
+      const char* const sb = dsm + rd + 4 * ff;
       for (int v = tid; v < n; v += nt) {
         const int2 r = __ldg(reinterpret_cast<const int2*>(g.d_vn_rec) + __ldg(g.d_vn_pos + v));
         float t = *reinterpret_cast<const float*>(sb + lo16(r.x)) + *reinterpret_cast<const float*>(sb + hi16(r.x));
@@ -395,7 +443,7 @@ __device__ __forceinline__ int direct_iteration_end(const DevGraph& g, const Dec
   unsigned mask = 0;
 #pragma unroll
   for (int ff = 0; ff < FV; ++ff) mask |= (ctl->done[ff] == 3 ? 1u : 0u) << ff;
-  direct_load_slots<FV>(g, a, ctl, mask);
+  direct_load_slots<FV, FLOOD>(g, a, ctl, mask);
   if (tid < FV && ctl->done[tid] == 3) ctl->done[tid] = 0;
   __syncthreads();
   return 1;
@@ -403,7 +451,8 @@ __device__ __forceinline__ int direct_iteration_end(const DevGraph& g, const Dec
 
 // State after a.max_subiters sub-iterations: c2v and v2c per CN-major edge id.
 template <int FV>
-__device__ __forceinline__ void direct_dump(const DevGraph& g, const DecodeArgs& a, const DirectCtl<FV>* ctl) {
+__device__ __forceinline__ void direct_dump(const DevGraph& g, const DecodeArgs& a, const DirectCtl<FV>* ctl,
+                                            uint32_t rd = 0) {  // rd: byte offset of the current edge cells
   const int tid = threadIdx.x, nt = blockDim.x, E = g.E;
   for (int ff = 0; ff < FV; ++ff) {
     const long long f = ctl->frame[ff];
@@ -414,9 +463,10 @@ __device__ __forceinline__ void direct_dump(const DevGraph& g, const DecodeArgs&
       const bool holder = hi16(r.x) != 0xffffu;
       const float l = holder ? *reinterpret_cast<const float*>(sb + hi16(r.x)) : 0.f;
       // a holder cell stores c2v + L (exact while c2v = 0)
-      if (a.c2v_out) a.c2v_out[f * E + e] = (*reinterpret_cast<const float*>(sb + lo16(r.x)) - l) * kLn2;
+      if (a.c2v_out) a.c2v_out[f * E + e] = (*reinterpret_cast<const float*>(sb + rd + lo16(r.x)) - l) * kLn2;
       if (a.v2c_out) {
-        float t = *reinterpret_cast<const float*>(sb + lo16(r.y)) + *reinterpret_cast<const float*>(sb + hi16(r.y));
+        float t = *reinterpret_cast<const float*>(sb + rd + lo16(r.y)) +
+                  *reinterpret_cast<const float*>(sb + rd + hi16(r.y));
         if (holder) t += l;
         a.v2c_out[f * E + e] = clamp_bits(t) * kLn2;
       }
@@ -424,8 +474,9 @@ __device__ __forceinline__ void direct_dump(const DevGraph& g, const DecodeArgs&
   }
 }
 
-template <int FV>
-__global__ void __launch_bounds__(kDirectThreads, direct_min_blocks<FV>())
+// FLOOD: one group in rounds over two copies of the edge cells (direct_flood_iteration)
+template <int FV, bool FLOOD>
+__global__ void __launch_bounds__(FLOOD ? kFloodThreads : kDirectThreads, FLOOD ? 2 : direct_min_blocks<FV>())
     decode_direct(const DevGraph g, const DecodeArgs a, unsigned long long* queue) {
   constexpr int CB = 4 * FV;  // cell bytes
   __shared__ DirectCtl<FV> ctl;
@@ -447,7 +498,7 @@ __global__ void __launch_bounds__(kDirectThreads, direct_min_blocks<FV>())
     for (int ff = 0; ff < FV; ++ff) any |= ctl.frame[ff] >= 0;
     if (!any) return;  // the queue was empty when this CTA started
   }
-  direct_load_slots<FV>(g, a, &ctl, (1u << FV) - 1);
+  direct_load_slots<FV, FLOOD>(g, a, &ctl, (1u << FV) - 1);
 
   // the thread's CN record one group ahead
   int cn = g.d_goff[1] - g.d_goff[0];
@@ -456,19 +507,42 @@ __global__ void __launch_bounds__(kDirectThreads, direct_min_blocks<FV>())
   const bool check = a.early_stop || a.trace;
   const int G = g.G;
 
-  if (a.max_subiters > 0) {  // state dump
-    for (int sub = 0, grp = 0; sub < a.max_subiters; ++sub, grp = grp + 1 < G ? grp + 1 : 0)
-      direct_group<FV>(g, tid, grp, cn, next_rec);
-    direct_dump<FV>(g, a, &ctl);
-    return;
-  }
-  for (int it_cta = 1;; ++it_cta) {
-    // one iteration for every slot (decoder.hpp:157-160)
-    for (int grp = 0; grp < G; ++grp) direct_group<FV>(g, tid, grp, cn, next_rec);
-    if (!check && it_cta < a.max_iters) continue;
-    const int r = direct_iteration_end<FV>(g, a, queue, &ctl, it_cta);
-    if (r == 2) break;
-    if (r == 1) it_cta = 0;
+  if constexpr (FLOOD) {
+    const uint32_t buf = static_cast<uint32_t>(g.d_buf_cells) * CB;
+    uint32_t rd = 0;  // the copy of the edge cells that holds the current messages
+    if (a.max_subiters > 0) {  // state dump: a sub-iteration is an iteration
+      for (int sub = 0; sub < a.max_subiters; ++sub) {
+        direct_flood_iteration<FV>(g, tid, nt, rd, buf - rd);
+        __syncthreads();
+        rd = buf - rd;
+      }
+      direct_dump<FV>(g, a, &ctl, rd);
+      return;
+    }
+    for (int it_cta = 1;; ++it_cta) {
+      direct_flood_iteration<FV>(g, tid, nt, rd, buf - rd);
+      __syncthreads();
+      rd = buf - rd;
+      if (!check && it_cta < a.max_iters) continue;
+      const int r = direct_iteration_end<FV, true>(g, a, queue, &ctl, it_cta, rd);
+      if (r == 2) break;
+      if (r == 1) it_cta = 0;
+    }
+  } else {
+    if (a.max_subiters > 0) {  // state dump
+      for (int sub = 0, grp = 0; sub < a.max_subiters; ++sub, grp = grp + 1 < G ? grp + 1 : 0)
+        direct_group<FV>(g, tid, grp, cn, next_rec);
+      direct_dump<FV>(g, a, &ctl);
+      return;
+    }
+    for (int it_cta = 1;; ++it_cta) {
+      // one iteration for every slot (decoder.hpp:157-160)
+      for (int grp = 0; grp < G; ++grp) direct_group<FV>(g, tid, grp, cn, next_rec);
+      if (!check && it_cta < a.max_iters) continue;
+      const int r = direct_iteration_end<FV, false>(g, a, queue, &ctl, it_cta, 0u);
+      if (r == 2) break;
+      if (r == 1) it_cta = 0;
+    }
   }
   if (tid == 0 && a.counters)
     for (int i = 0; i < 6; ++i)
@@ -477,7 +551,10 @@ __global__ void __launch_bounds__(kDirectThreads, direct_min_blocks<FV>())
 
 using DirectFn = void (*)(const DevGraph, const DecodeArgs, unsigned long long*);
 
-DirectFn pick_direct(int fv) { return fv == 4 ? decode_direct<4> : (fv == 2 ? decode_direct<2> : nullptr); }
+DirectFn pick_direct(int fv, bool flood) {
+  if (flood) return fv == 2 ? decode_direct<2, true> : nullptr;
+  return fv == 4 ? decode_direct<4, false> : (fv == 2 ? decode_direct<2, false> : nullptr);
+}
 
 }  // namespace
 
@@ -491,7 +568,9 @@ Plan plan_direct(const DevGraph& g, int64_t frames) {
   Plan p;
   const int fv = g.d_fv;
   if ((fv != 2 && fv != 4) || !g.d_cn_rec || g.per_frame) return p;
-  if (g.d_max_items > kDirectThreads) return p;  // one CN item per thread
+  const bool flood = g.d_buf_cells > 0;
+  if (flood && fv != 2) return p;
+  if (!flood && g.d_max_items > kDirectThreads) return p;  // one CN item per thread
   size_t bytes = static_cast<size_t>(g.d_cells) * 4 * fv + ((g.n + 15) & ~15);
   if (const char* e = std::getenv("LDPCB_DIRECT_PAD")) bytes += std::atoi(e);  // occupancy experiments
   int dev = 0, optin = 0;
@@ -501,7 +580,7 @@ Plan plan_direct(const DevGraph& g, int64_t frames) {
   p.kernel = 3;
   p.fpc = fv;
   p.fv = fv;
-  p.threads = std::max(64, std::min(kDirectThreads, (g.d_max_items + 31) / 32 * 32));
+  p.threads = flood ? kFloodThreads : std::max(64, std::min(kDirectThreads, (g.d_max_items + 31) / 32 * 32));
   p.smem = static_cast<int>(bytes);
   p.degree_bucket = 6;
   p.ctas = (frames + p.fpc - 1) / p.fpc;
@@ -513,7 +592,7 @@ int launch_direct(const DevGraph& g, const DecodeArgs& a, void* stream, Plan* us
   if (used) *used = p;
   if (p.kernel != 3) return static_cast<int>(cudaErrorInvalidConfiguration);
   if (a.frames <= 0) return 0;
-  DirectFn fn = pick_direct(g.d_fv);
+  DirectFn fn = pick_direct(g.d_fv, g.d_buf_cells > 0);
   cudaError_t err =
       cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, p.smem);
   if (err != cudaSuccess) return static_cast<int>(err);

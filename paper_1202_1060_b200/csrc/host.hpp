@@ -174,6 +174,8 @@ struct DirectTables {
   int fv = 2;        // frames per cell (2: 8-byte cells, 4: 16-byte cells)
   int cells = 0;     // cells, multiple of 16
   int l_base = 0;    // L cell of position p = l_base + p
+  int buf_cells = 0; // flooding (one group of more CNs than a CTA has threads): the edge cells exist twice,
+                     // buffer 1 = buffer 0 + buf_cells; an iteration reads one and writes the other. 0: one buffer
   int max_items = 0;
   std::vector<int32_t> cn_off, cn_rec, vn_rec, vn_hold, all_cn, edge_rec, vn_pos;
 };

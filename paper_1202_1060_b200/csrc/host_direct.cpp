@@ -107,9 +107,15 @@ DirectTables direct_tables(const CodeData& c, const ScheduleData& s, int fv) {
   for (int v = 0; v < c.n; ++v)
     if (c.var_off[v + 1] - c.var_off[v] != 3) return t;
   const int E = c.E, n = c.n;
-  const int l_base = (E + 15) / 16 * 16;
+  // One group of more CNs than a CTA has threads (flooding): its CN items run in several
+  // rounds, so the Jacobi order needs the old messages kept while new ones are written:
+  // two copies of the edge cells, read one / write the other, swapped every iteration.
+  const bool flood = s.G == 1 && s.grp_off[1] - s.grp_off[0] > 96;
+  const int e_cells = (E + 15) / 16 * 16;
+  const int l_base = flood ? 2 * e_cells : e_cells;
   const int cells = l_base + (n + 15) / 16 * 16;
   if (static_cast<long long>(cells) * cell_bytes > 65536) return t;
+  t.buf_cells = flood ? e_cells : 0;
   const std::vector<int> hold = holder_edges(c);
   if (hold.empty()) return t;
   // groups without repeated CNs (a second update of a CN inside a group would

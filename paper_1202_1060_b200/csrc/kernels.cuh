@@ -34,7 +34,7 @@ struct DevGraph {
   const uint32_t* fix_fresh = nullptr;  // per fix_rec record
   bool covers = false;
   // direct (posterior-free) kernel tables (host.hpp DirectTables); d_fv = 0: none
-  int d_fv = 0, d_cells = 0, d_l_base = 0, d_max_items = 0;
+  int d_fv = 0, d_cells = 0, d_l_base = 0, d_max_items = 0, d_buf_cells = 0;
   // first CN record of every group, a kernel parameter (constant bank): group
   // ranges then cost a uniform constant load, no vector register
   static constexpr int kDirectMaxGroups = 96;

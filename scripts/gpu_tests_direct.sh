@@ -1,2 +1,4 @@
 #!/bin/bash
-python -m pytest tests -m gpu -q --durations=5 -k "direct or tuning or cpp or sweep or multi or per_frame or pins" 2>&1 | tail -25
+python -m pytest tests -m gpu -q -x --durations=5 -k "not c4_long and not stream" 2>&1 | tail -12
+AB_KERNEL=1 python scripts/ab_speed.py 2>&1 | grep " bp "
+AB_KERNEL=0 python scripts/ab_speed.py 2>&1 | grep frames/s | cut -c1-120

@@ -653,18 +653,21 @@ def test_fix16_records_are_bit_identical(P, torch, orc, case):
 
 
 # ----------------------------------------- posterior-free resident kernel ----
-@pytest.mark.parametrize("sched", ["ndgsbp", "gsbp"])
+@pytest.mark.parametrize("sched", ["ndgsbp", "gsbp", "bp"])
 def test_direct_kernel_is_the_default_and_matches_the_posterior_kernel(P, torch, orc, sched):
-    """C1 under NDGSBP / GSBP decodes on the posterior-free kernel (direct.cu:
-    plan kernel 22); flooding (504 CNs in one group) keeps the posterior-based
-    one. Against that kernel and the reference: >= 99.9 % identical frames
+    """C1 under NDGSBP / GSBP / flooding decodes on the posterior-free kernel
+    (direct.cu: plan kernel 22; flooding runs its 504 CNs in rounds over two
+    copies of the edge cells); groups of more than 96 CNs that are not the
+    only group keep the posterior-based one. Against that kernel and the
+    reference: >= 99.9 % identical frames
     with early stop and at fixed 10 iterations, posteriors within 1e-3,
     identical traces on identical frames, counters equal to the outputs."""
     g = P.configs.c1_code()
     sch = P.configs.c1_schedules(g)
     s = sch[sched]
     assert P.plan(g, s, 1000)["kernel"] == 22
-    assert P.plan(g, sch["bp"], 1000)["kernel"] == 12
+    assert P.plan(g, sch["bp"], 1000)["kernel"] == 22
+    assert P.plan(g, P.GroupSchedule.windows(g, 4, 126, 126, P.DISJOINT), 1000)["kernel"] == 12
     F = 6001
     llr_h = orc.transmit_batch_f32(P.sigma2_from_ebn0(1.75, g.rate), 11, g.n_vars, 0, F, THREADS)
     llr = cu(torch, llr_h)
@@ -702,17 +705,19 @@ def test_direct_kernel_ragged_batches_and_forced_selection(P, torch, orc):
     sch = P.configs.c1_schedules(g)
     s = sch["ndgsbp"]
     llr = cu(torch, orc.transmit_batch_f32(P.sigma2_from_ebn0(1.5, g.rate), 4, g.n_vars, 0, 2501, THREADS))
-    for es, iters in ((True, 20), (False, 7)):
-        base = to_np(P.decode_batch(g, s, llr, iters, early_stop=es, posterior=True, trace=True))
-        for F in (1, 2, 3, 13, 777):
-            part = to_np(P.decode_batch(g, s, llr[:F].contiguous(), iters, early_stop=es, posterior=True, trace=True))
-            for k in part:
-                assert np.array_equal(part[k], base[k][:F]), (es, F, k)
+    for name in ("ndgsbp", "bp"):
+        for es, iters in ((True, 20), (False, 7)):
+            base = to_np(P.decode_batch(g, sch[name], llr, iters, early_stop=es, posterior=True, trace=True))
+            for F in (1, 2, 3, 13, 777):
+                part = to_np(P.decode_batch(g, sch[name], llr[:F].contiguous(), iters, early_stop=es, posterior=True,
+                                            trace=True))
+                for k in part:
+                    assert np.array_equal(part[k], base[k][:F]), (name, es, F, k)
     P.set_kernel(3)
     try:
         forced = to_np(P.decode_batch(g, s, llr[:64].contiguous(), 20, posterior=True))
-        with pytest.raises(Exception):
-            P.decode_batch(g, sch["bp"], llr[:64].contiguous(), 20)
+        with pytest.raises(Exception):  # four groups of 126 CNs: more than one CN item per thread
+            P.decode_batch(g, P.GroupSchedule.windows(g, 4, 126, 126, P.DISJOINT), llr[:64].contiguous(), 20)
     finally:
         P.set_kernel(0)
     auto = to_np(P.decode_batch(g, s, llr[:64].contiguous(), 20, posterior=True))
