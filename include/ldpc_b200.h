@@ -110,6 +110,17 @@ int ldpcb_schedule_dims(ldpcb_schedule s, int32_t *kind, int32_t *n_groups, int3
                         double *overlap, int64_t *edge_updates_per_iter, int64_t *touched_per_iter);
 int ldpcb_schedule_export(ldpcb_schedule s, int32_t *grp_off, int32_t *grp_cns);
 int ldpcb_schedule_iteration_budget(ldpcb_schedule s, int i_max, int32_t *budget); /* :206-210 */
+/* Layout of the posterior-free resident kernel for this schedule:
+ * frames per thread (0: the kernel does not apply to this code / schedule),
+ * cells per CTA, first L cell, cells between the two edge-cell copies (flooding;
+ * 0 otherwise), CN items over all groups, shared-memory wavefronts per access
+ * after bank colouring. ldpcb_schedule_direct_export copies the tables:
+ * cn_off[G+1], cn_rec[12 * items], vn_rec[2 n], vn_hold[n], vn_pos[n],
+ * edge_rec[2 E] (byte offsets; formats in csrc/host.hpp DirectTables). */
+int ldpcb_schedule_direct_layout(ldpcb_schedule s, int32_t *frames_per_thread, int32_t *cells, int32_t *l_base,
+                                 int32_t *buffer_cells, int32_t *n_items, double *wavefronts_per_access);
+int ldpcb_schedule_direct_export(ldpcb_schedule s, int32_t *cn_off, int32_t *cn_rec, int32_t *vn_rec,
+                                 int32_t *vn_hold, int32_t *vn_pos, int32_t *edge_rec);
 int ldpcb_schedule_cocsg(ldpcb_schedule s, int32_t *counts /* n_groups-1 */);       /* :175-201 */
 void ldpcb_schedule_destroy(ldpcb_schedule s);
 

@@ -55,6 +55,8 @@ _SIGS = {
     "ldpcb_schedule_dims": (C.c_int, [vp, P32, P32, P32, P32, PD, P64, P64]),
     "ldpcb_schedule_export": (C.c_int, [vp, vp, vp]),
     "ldpcb_schedule_iteration_budget": (C.c_int, [vp, C.c_int, P32]),
+    "ldpcb_schedule_direct_layout": (C.c_int, [vp, P32, P32, P32, P32, P32, PD]),
+    "ldpcb_schedule_direct_export": (C.c_int, [vp, vp, vp, vp, vp, vp, vp]),
     "ldpcb_schedule_cocsg": (C.c_int, [vp, vp]),
     "ldpcb_schedule_destroy": (None, [vp]),
     "ldpcb_sigma2_from_ebn0": (C.c_int, [dbl, dbl, PD]),

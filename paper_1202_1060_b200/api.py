@@ -284,6 +284,26 @@ class GroupSchedule:
                                                          out.data_ptr(), _stream()))
         return out.view(torch.uint16).to(torch.int32) if hasattr(torch, "uint16") else (out.to(torch.int32) & 0xFFFF)
 
+    def direct_layout(self) -> dict | None:
+        """Tables of the posterior-free resident kernel for this schedule (csrc/host.hpp
+        DirectTables), or None where that kernel does not apply: frames per thread, cell
+        counts, wavefronts per shared-memory access after bank colouring, and the records
+        (byte offsets into the cell array)."""
+        fv, cells, lb, buf, items = (C.c_int32() for _ in range(5))
+        wf = C.c_double()
+        check(lib.ldpcb_schedule_direct_layout(self._h, fv, cells, lb, buf, items, wf))
+        if fv.value == 0:
+            return None
+        g = self.graph
+        out = {"frames_per_thread": fv.value, "cells": cells.value, "l_base": lb.value, "buffer_cells": buf.value,
+               "wavefronts_per_access": wf.value,
+               "cn_off": np.empty(self.n_groups + 1, np.int32), "cn_rec": np.empty(12 * items.value, np.int32),
+               "vn_rec": np.empty(2 * g.n_vars, np.int32), "vn_hold": np.empty(g.n_vars, np.int32),
+               "vn_pos": np.empty(g.n_vars, np.int32), "edge_rec": np.empty(2 * g.n_edges, np.int32)}
+        check(lib.ldpcb_schedule_direct_export(self._h, *(_vp(out[k]) for k in
+                                                          ("cn_off", "cn_rec", "vn_rec", "vn_hold", "vn_pos", "edge_rec"))))
+        return out
+
     def iteration_budget(self, i_max: int) -> int:
         b = C.c_int32()
         check(lib.ldpcb_schedule_iteration_budget(self._h, i_max, C.byref(b)))

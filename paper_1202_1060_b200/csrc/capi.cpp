@@ -1068,6 +1068,40 @@ int ldpcb_decode_plan(ldpcb_code code, ldpcb_schedule s, int64_t frames, int32_t
   });
 }
 
+int ldpcb_schedule_direct_layout(ldpcb_schedule s, int32_t* frames_per_thread, int32_t* cells, int32_t* l_base,
+                                 int32_t* buffer_cells, int32_t* n_items, double* wavefronts_per_access) {
+  return guard([&] {
+    need(s != nullptr, "null handle");
+    const auto& t = s->impl->direct;
+    if (frames_per_thread) *frames_per_thread = t.ok ? t.fv : 0;
+    if (cells) *cells = t.ok ? t.cells : 0;
+    if (l_base) *l_base = t.ok ? t.l_base : 0;
+    if (buffer_cells) *buffer_cells = t.ok ? t.buf_cells : 0;
+    if (n_items) *n_items = t.ok ? t.cn_off.back() : 0;
+    if (wavefronts_per_access) *wavefronts_per_access = t.ok ? t.wavefronts : 0.0;
+    return LDPCB_OK;
+  });
+}
+
+int ldpcb_schedule_direct_export(ldpcb_schedule s, int32_t* cn_off, int32_t* cn_rec, int32_t* vn_rec,
+                                 int32_t* vn_hold, int32_t* vn_pos, int32_t* edge_rec) {
+  return guard([&] {
+    need(s != nullptr, "null handle");
+    const auto& t = s->impl->direct;
+    need(t.ok, "the posterior-free kernel does not apply to this schedule");
+    auto put = [](int32_t* out, const std::vector<int32_t>& v) {
+      if (out) std::copy(v.begin(), v.end(), out);
+    };
+    put(cn_off, t.cn_off);
+    put(cn_rec, t.cn_rec);
+    put(vn_rec, t.vn_rec);
+    put(vn_hold, t.vn_hold);
+    put(vn_pos, t.vn_pos);
+    put(edge_rec, t.edge_rec);
+    return LDPCB_OK;
+  });
+}
+
 int ldpcb_set_tuning(int frames_per_cta, int threads) {
   return guard([&] {
     need(frames_per_cta == 0 || frames_per_cta == 1 || frames_per_cta == 2 || frames_per_cta == 4 ||

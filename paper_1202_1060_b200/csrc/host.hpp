@@ -177,6 +177,7 @@ struct DirectTables {
   int buf_cells = 0; // flooding (one group of more CNs than a CTA has threads): the edge cells exist twice,
                      // buffer 1 = buffer 0 + buf_cells; an iteration reads one and writes the other. 0: one buffer
   int max_items = 0;
+  double wavefronts = 0.0;  // shared-memory wavefronts per half-warp access after bank colouring (1 = conflict-free)
   std::vector<int32_t> cn_off, cn_rec, vn_rec, vn_hold, all_cn, edge_rec, vn_pos;
 };
 DirectTables direct_tables(const CodeData& c, const ScheduleData& s, int fv);

@@ -212,6 +212,7 @@ DirectTables direct_tables(const CodeData& c, const ScheduleData& s, int fv) {
   for (int e = 0; e < E; ++e) edge_access(e, +1);
   const long long cost0 = sc.total;
   const int nsets = static_cast<int>(sc.mx.size());
+  t.wavefronts = nsets ? static_cast<double>(cost0) / nsets : 1.0;
   std::vector<int> at(E);  // edge at record position k of CN r
   for (int e = 0; e < E; ++e) at[c.row_off[row_of[e]] + pos[e]] = e;
   if (E + n <= 32768 && nsets > 0) {
@@ -313,6 +314,7 @@ DirectTables direct_tables(const CodeData& c, const ScheduleData& s, int fv) {
       }
     }
     if (sc.total > best_total) colour = best_colour, pos = best_pos, rd = best_rd;
+    t.wavefronts = static_cast<double>(std::min(sc.total, best_total)) / nsets;
     if (std::getenv("LDPCB_BANK_DEBUG"))
       std::fprintf(stderr, "direct_tables: %d sets, cost %.3f -> %.3f per set (%lld moves)\n", nsets,
                    static_cast<double>(cost0) / nsets, static_cast<double>(std::min(sc.total, best_total)) / nsets,
