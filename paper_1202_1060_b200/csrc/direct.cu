@@ -51,6 +51,9 @@ namespace {
 
 using namespace dev;
 
+#ifndef LDPCB_DIRECT_MINB
+#define LDPCB_DIRECT_MINB 5  // A/B: -DLDPCB_DIRECT_MINB=6
+#endif
 constexpr int kDirectThreads = 96;  // C1 NDGSBP: 84 CN items per group
 constexpr int kFloodThreads = 256;  // flooding: 504 CN items per iteration in two rounds; two CTAs per SM at 128 registers
                                     // (18 warps per SM would cap the kernel at 96 registers: 88 bytes of spills)
@@ -61,8 +64,14 @@ constexpr int kFloodThreads = 256;  // flooding: 504 CN items per iteration in t
 // and cost an address add per access).
 extern __shared__ __align__(16) char dsm[];
 
-// resident CTAs per SM the register budget is sized for: shared memory fits
-// six 2-frame CTAs (33 KB) or three 4-frame CTAs (66 KB). A seventh 2-frame
+// Resident CTAs per SM the register budget is sized for. Shared memory fits
+// six 2-frame CTAs (33 KB), but six 96-thread CTAs are 18 warps, five on
+// some SM sub-partition, which caps the kernel at 96 registers: ptxas then
+// re-issues FMNMX + EX2 for two of a CN item's six inputs where their z is
+// needed again (40 MUFU per item instead of 36) and spills 16 bytes. Sized
+// for five CTAs (15 warps, 112 registers, no re-issue, no spill) the C5 step
+// takes 98.96 ms against 102.85 (64-thread launches, GSBP, still run six
+// CTAs per SM). Three 4-frame CTAs (66 KB) with four frames per thread. A seventh 2-frame
 // CTA was tried (all control state moved to global memory so that the
 // kernel's shared memory is exactly the 32256-byte state): the 16 K registers
 // of an SM sub-partition hold five 96-register warps, so 21 warps per SM need
@@ -70,7 +79,7 @@ extern __shared__ __align__(16) char dsm[];
 // than six CTAs (108.3 against 104.1 ms per 2^21 frames).
 template <int FV>
 constexpr int direct_min_blocks() {
-  return FV == 2 ? 6 : 3;
+  return FV == 2 ? LDPCB_DIRECT_MINB : 3;
 }
 
 // one cell: FV frames as FV / 2 packed pairs
