@@ -1,5 +1,5 @@
 #!/bin/bash
-# A/B of two builds of the posterior-free resident kernel on the C5 n=1008 bench workload.
+# A/B of variants of the posterior-free resident kernel on the C5 n=1008 bench workload.
 mkdir -p gpurun_out
 B="python bench.py --workload c5_n1008 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e"
 run() { # label, env...
@@ -9,8 +9,8 @@ import sys, json
 for l in sys.stdin:
     if l.startswith('{'):
         d = json.loads(l)
-        print('$label', 'ms', round(d['ms_per_step'], 3), 'frac', round(d['roofline']['frac'], 4), 'FER', d['counters']['frame_errors'] / d['counters']['frames'], 'BE', d['counters']['bit_errors'])
+        print('$label', 'ms', round(d['ms_per_step'], 3), 'frac', round(d['roofline']['frac'], 4), 'FER', d['counters']['frame_errors'] / d['counters']['frames'], 'BE', d['counters']['bit_errors'], d['config']['plan'])
 " || tail -3 gpurun_out/ab_err.log
 }
-run "direct 6 CTAs/SM, 96 registers" X=1
-run "direct 5 CTAs/SM, 112 registers (no EX2 re-issue)" LDPCB_LIBRARY=paper_1202_1060_b200/libldpc_b200_minb5.so
+run "direct, versioned cells (one barrier per group)" X=1
+run "direct, two barriers per group" LDPCB_DIRECT_VERSIONED=0
