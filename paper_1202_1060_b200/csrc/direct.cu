@@ -149,7 +149,7 @@ __device__ __forceinline__ uint32_t hi16(int w) { return static_cast<uint32_t>(w
 // cn: the CNs of this group; next_rec: the thread's record for this group
 // (requested one group ahead). On return they describe the next group.
 template <int FV>
-__device__ __forceinline__ void direct_group(const DevGraph& g, int tid, int grp, int& cn, DRec& next_rec) {
+__device__ __forceinline__ void direct_group(const DevGraph& g, int tid, int grp, int& cn, int2& nx, DRec& next_rec) {
   const int G = g.G;
   const bool has = tid < cn;
   Cell<FV> x[6], lh[2];
@@ -176,9 +176,14 @@ __device__ __forceinline__ void direct_group(const DevGraph& g, int tid, int grp
   }
   // the next group's record, requested behind this group's shared-memory
   // loads a whole group before use
-  const int gn = grp + 1 < G ? grp + 1 : 0;
-  const int n0 = g.d_goff[gn], ncn = g.d_goff[gn + 1] - n0;
+  // (nx = its first record and CN count, read from the constant bank a group ago:
+  // the record's address must not wait for that read)
+  const int n0 = nx.x, ncn = nx.y;
   if (tid < ncn) next_rec.load(g.d_cn_rec + static_cast<size_t>(n0 + tid) * 12);
+  int gg = grp + 2;
+  gg -= gg >= G ? G : 0;
+  gg -= gg >= G ? G : 0;
+  nx = make_int2(g.d_goff[gg], g.d_goff[gg + 1] - g.d_goff[gg]);
   __syncthreads();  // every load of the group precedes every store
   if (has) {
     if constexpr (FV == 2) {  // every output stored as the boxplus emits it
@@ -513,6 +518,8 @@ __global__ void __launch_bounds__(FLOOD ? kFloodThreads : kDirectThreads, FLOOD 
   int cn = g.d_goff[1] - g.d_goff[0];
   DRec next_rec;
   if (tid < cn) next_rec.load(g.d_cn_rec + static_cast<size_t>(g.d_goff[0] + tid) * 12);
+  const int g1 = g.G > 1 ? 1 : 0;
+  int2 nx = make_int2(g.d_goff[g1], g.d_goff[g1 + 1] - g.d_goff[g1]);  // the group after the first
   const bool check = a.early_stop || a.trace;
   const int G = g.G;
 
@@ -540,13 +547,13 @@ __global__ void __launch_bounds__(FLOOD ? kFloodThreads : kDirectThreads, FLOOD 
   } else {
     if (a.max_subiters > 0) {  // state dump
       for (int sub = 0, grp = 0; sub < a.max_subiters; ++sub, grp = grp + 1 < G ? grp + 1 : 0)
-        direct_group<FV>(g, tid, grp, cn, next_rec);
+        direct_group<FV>(g, tid, grp, cn, nx, next_rec);
       direct_dump<FV>(g, a, &ctl);
       return;
     }
     for (int it_cta = 1;; ++it_cta) {
       // one iteration for every slot (decoder.hpp:157-160)
-      for (int grp = 0; grp < G; ++grp) direct_group<FV>(g, tid, grp, cn, next_rec);
+      for (int grp = 0; grp < G; ++grp) direct_group<FV>(g, tid, grp, cn, nx, next_rec);
       if (!check && it_cta < a.max_iters) continue;
       const int r = direct_iteration_end<FV, false>(g, a, queue, &ctl, it_cta, 0u);
       if (r == 2) break;

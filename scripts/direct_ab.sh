@@ -1,5 +1,5 @@
 #!/bin/bash
-# A/B of variants of the posterior-free resident kernel on the C5 n=1008 bench workload.
+# The posterior-free resident kernel on the C5 n=1008 bench workload (A/B of builds via LDPCB_LIBRARY).
 mkdir -p gpurun_out
 B="python bench.py --workload c5_n1008 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e"
 run() { # label, env...
@@ -12,5 +12,6 @@ for l in sys.stdin:
         print('$label', 'ms', round(d['ms_per_step'], 3), 'frac', round(d['roofline']['frac'], 4), 'FER', d['counters']['frame_errors'] / d['counters']['frames'], 'BE', d['counters']['bit_errors'], d['config']['plan'])
 " || tail -3 gpurun_out/ab_err.log
 }
-run "direct, versioned cells (one barrier per group)" X=1
-run "direct, two barriers per group" LDPCB_DIRECT_VERSIONED=0
+run "direct" X=1
+[ -n "$AB_BASE" ] && run "direct (base library $AB_BASE)" LDPCB_LIBRARY=$AB_BASE
+true
