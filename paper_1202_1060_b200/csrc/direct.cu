@@ -155,6 +155,10 @@ __device__ __forceinline__ void direct_group(const DevGraph& g, int tid, int grp
   Cell<FV> x[6], lh[2];
   uint32_t own[6];
   const DRec cur = next_rec;
+  // the next group's record, requested a whole group before use (nx = its first
+  // record and CN count, read from the constant bank a group ago)
+  if (tid < nx.y) next_rec.load(g.d_cn_rec + static_cast<size_t>(nx.x + tid) * 12);
+  const int ncn = nx.y;
   if (has) {
     const int4 ra = cur.a, rb = cur.b;
     const int2 rc = cur.c;
@@ -174,12 +178,6 @@ __device__ __forceinline__ void direct_group(const DevGraph& g, int tid, int grp
       x[2 + j] = add_cell<FV>(ld_cell<FV>(dsm, field(3 * j + 1)), ld_cell<FV>(dsm, field(3 * j + 2)));
     }
   }
-  // the next group's record, requested behind this group's shared-memory
-  // loads a whole group before use
-  // (nx = its first record and CN count, read from the constant bank a group ago:
-  // the record's address must not wait for that read)
-  const int n0 = nx.x, ncn = nx.y;
-  if (tid < ncn) next_rec.load(g.d_cn_rec + static_cast<size_t>(n0 + tid) * 12);
   int gg = grp + 2;
   gg -= gg >= G ? G : 0;
   gg -= gg >= G ? G : 0;
