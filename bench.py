@@ -39,9 +39,9 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 # Shared-memory bank colouring of the resident kernel's tables (host-side, once
-# per schedule handle, outside every timed region): 16000 annealing moves per CN
-# (about 6 s for the C1 schedule) instead of the library default of 4000.
-os.environ.setdefault("LDPCB_BANK_ITERS", "16000")
+# per schedule handle, outside every timed region): 40000 annealing moves per CN
+# (about 15 s per table set of the C1 schedule) instead of the library default of 4000.
+os.environ.setdefault("LDPCB_BANK_ITERS", "40000")
 
 METRIC = "decoded info bits/s at fixed iterations"
 UNIT = "info bits/s"
