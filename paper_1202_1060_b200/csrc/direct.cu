@@ -347,23 +347,29 @@ __device__ __forceinline__ int direct_iteration_end(const DevGraph& g, const Dec
   const uint32_t rd = FLOOD ? rd_flood : 0u;
   constexpr int CB = 4 * FV;
   const int tid = threadIdx.x, nt = blockDim.x, n = g.n, m = g.m;
-  uint8_t* const s_hd = reinterpret_cast<uint8_t*>(dsm + static_cast<size_t>(g.d_cells) * CB);  // [n] bit i = frame i
+  // hard-decision bytes [n], bit i = frame i: byte offset hd in the CTA's shared memory. Everything below
+  // addresses dsm[integer offset], which compiles to LDS [R + uniform base] as in the sub-iteration loop
+  // (a derived pointer costs a generic-to-shared conversion and an address add per access).
+  const uint32_t hd = static_cast<uint32_t>(g.d_cells) * CB;
+  const uint8_t* const s_hd = reinterpret_cast<const uint8_t*>(dsm) + hd;
   const int nb = (n + 7) >> 3;
   const bool check = a.early_stop || a.trace;
   // hard decisions (tie -> 0) from the totals ((c2v_h + L) + c2v) + c2v, one sign bit per frame
+#pragma unroll 2
   for (int pos = tid; pos < n; pos += nt) {
     const int2 r = __ldg(reinterpret_cast<const int2*>(g.d_vn_rec) + pos);
-    Cell<FV> t = add_cell<FV>(ld_cell<FV>(dsm + rd, lo16(r.x)), ld_cell<FV>(dsm + rd, hi16(r.x)));
-    t = add_cell<FV>(t, ld_cell<FV>(dsm + rd, lo16(r.y)));
-    s_hd[pos] = static_cast<uint8_t>(sign_bits<FV>(t));
+    Cell<FV> t = add_cell<FV>(ld_cell<FV>(dsm, lo16(r.x) + rd), ld_cell<FV>(dsm, hi16(r.x) + rd));
+    t = add_cell<FV>(t, ld_cell<FV>(dsm, lo16(r.y) + rd));
+    dsm[hd + pos] = static_cast<char>(sign_bits<FV>(t));
   }
   __syncthreads();
   {  // syndrome weight (decoder.hpp:129-137)
     int w[FV] = {};
+#pragma unroll 2
     for (int r = tid; r < m; r += nt) {
       const int4 q = __ldg(reinterpret_cast<const int4*>(g.d_all_cn) + r);
-      const unsigned x = s_hd[lo16(q.x)] ^ s_hd[hi16(q.x)] ^ s_hd[lo16(q.y)] ^ s_hd[hi16(q.y)] ^ s_hd[lo16(q.z)] ^
-                         s_hd[hi16(q.z)];
+      auto b = [&](uint32_t v) { return static_cast<unsigned>(static_cast<uint8_t>(dsm[hd + v])); };
+      const unsigned x = b(lo16(q.x)) ^ b(hi16(q.x)) ^ b(lo16(q.y)) ^ b(hi16(q.y)) ^ b(lo16(q.z)) ^ b(hi16(q.z));
 #pragma unroll
       for (int i = 0; i < FV; ++i) w[i] += (x >> i) & 1u;
     }
