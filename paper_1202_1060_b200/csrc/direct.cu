@@ -142,6 +142,15 @@ struct DRec {
   }
 };
 
+// channel LLRs are read once: keep them out of L1, where the record tables live
+__device__ __forceinline__ float4 ldg_stream(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ uint32_t lo16(int w) { return static_cast<uint32_t>(w) & 0xffffu; }
 __device__ __forceinline__ uint32_t hi16(int w) { return static_cast<uint32_t>(w) >> 16; }
 
@@ -313,7 +322,7 @@ __device__ __forceinline__ void direct_load_slots(const DevGraph& g, const Decod
 #pragma unroll
         for (int u = 0; u < U; ++u)
           if (b0 + u * nt < n / 4)
-            x[u] = __ldg(l4 + b0 + u * nt), p[u] = __ldg(p4 + b0 + u * nt), h[u] = __ldg(h4 + b0 + u * nt);
+            x[u] = ldg_stream(l4 + b0 + u * nt), p[u] = __ldg(p4 + b0 + u * nt), h[u] = __ldg(h4 + b0 + u * nt);
 #pragma unroll
         for (int u = 0; u < U; ++u)
           if (b0 + u * nt < n / 4) {
