@@ -30,8 +30,9 @@ using namespace dev;
 // Lane states (done[]): bit 0 set = the lane is not decoding. Chunk mode
 // uses 0 / 1; the frame queue adds 2 = decoding the first iteration of a
 // frame it was refilled with ("fresh", host.hpp KernelTables::cn_fresh) and
-// 3 = retiring (stopped this iteration, outputs pending).
-enum LaneState : int { kLive = 0, kIdle = 1, kFresh = 2, kRetiring = 3 };
+// 3 = retiring (stopped this iteration, outputs pending), 5 = waiting (outputs
+// written, to be refilled at the next refill iteration).
+enum LaneState : int { kLive = 0, kIdle = 1, kFresh = 2, kRetiring = 3, kWaiting = 5 };
 
 struct ChunkState {
   int64_t B = 0;     // layout stride (frames), multiple of 4
@@ -50,7 +51,8 @@ struct ChunkState {
   unsigned* sw = nullptr;             // [n][B/32] hard-decision sign words
   unsigned* fail = nullptr;           // [B/32] lanes failing some parity check (no-trace syndrome test), or null
   int* list = nullptr;                // [B] lanes retiring this iteration
-  int* ctl = nullptr;                 // [0] retiring lanes, [1] lanes decoding
+  int* wlist = nullptr;               // [B] lanes waiting for a refill
+  int* ctl = nullptr;                 // [0] retiring lanes, [1] lanes decoding, [2] waiting lanes
   unsigned long long* next = nullptr; // next frame id to hand out
 };
 
@@ -732,13 +734,16 @@ __global__ void stream_q_setup(ChunkState s, int64_t frames) {
     *s.next = static_cast<unsigned long long>(s.nb);
     s.ctl[0] = 0;
     s.ctl[1] = s.nb;
+    s.ctl[2] = 0;
   }
 }
 
 // Per-lane bookkeeping after the syndrome test (decoder.hpp:166-177).
-__global__ void stream_q_iter_end(ChunkState s, int early_stop, int32_t* trace, int max_iters) {
+// reset_wait: the previous iteration refilled every waiting lane.
+__global__ void stream_q_iter_end(ChunkState s, int early_stop, int32_t* trace, int max_iters, int reset_wait) {
   pdl_enter();
   const int64_t f = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (f == 0 && reset_wait) s.ctl[2] = 0;
   if (f >= s.B || (s.done[f] & 1)) return;
   // lane f = 4 (32 W + b) + i is bit b of word 4 W + i (the sign-word layout)
   const int w = s.fail ? static_cast<int>((s.fail[4 * (f / 128) + (f & 3)] >> ((f >> 2) & 31)) & 1u) : s.weight[f];
@@ -754,15 +759,48 @@ __global__ void stream_q_iter_end(ChunkState s, int early_stop, int32_t* trace, 
   }
 }
 
-// Outputs of the retiring lanes (sim.hpp:119-123) and their refill with the
-// next frames; one block per retiring lane at a time.
+// A lane takes the next frame of the batch (or goes idle): init_state
+// (decoder.hpp:39-52) of the new frame writes L only (fresh bits).
+__device__ __forceinline__ void stream_q_refill(const DevGraph& g, const ChunkState& s, const float* __restrict__ llr,
+                                                int64_t frames, int64_t f, long long* s_new) {
+  const int n = g.n;
+  if (threadIdx.x == 0) {
+    const unsigned long long nf = atomicAdd(s.next, 1ull);
+    *s_new = nf < static_cast<unsigned long long>(frames) ? static_cast<long long>(nf) : -1ll;
+    s.frame[f] = *s_new;
+  }
+  __syncthreads();
+  const long long nf = *s_new;
+  if (nf >= 0) {
+    const float* row = llr + nf * n;
+    for (int v = threadIdx.x; v < n; v += blockDim.x)
+      s.L[static_cast<int64_t>(__ldg(g.vn_pos + v)) * s.B + f] = clamp_llr(__ldg(row + v)) * kLog2e;
+  }
+  if (threadIdx.x == 0) {
+    s.iters[f] = 0;
+    s.conv[f] = 0;
+    s.weight[f] = 0;
+    if (nf >= 0) {
+      s.done[f] = kFresh;
+    } else {
+      s.done[f] = kIdle;
+      atomicSub(s.ctl + 1, 1);
+    }
+  }
+  __syncthreads();
+}
+
+// Outputs of the retiring lanes (sim.hpp:119-123); one block per retiring
+// lane at a time. refill: the lanes that stopped now or in earlier iterations
+// (the waiting list) take the next frames; otherwise a stopped lane waits, so
+// that the iterations in between run the kernels without fresh-frame code.
 __global__ void __launch_bounds__(256) stream_q_retire(const DevGraph g, ChunkState s, const DecodeArgs a,
-                                                        const float* __restrict__ llr, int64_t frames) {
+                                                        const float* __restrict__ llr, int64_t frames, int refill) {
   pdl_enter();
   __shared__ int s_errs;
   __shared__ long long s_new;
   const int n = g.n, nbytes = (n + 7) / 8;
-  const int count = s.ctl[0];
+  const int count = s.ctl[0], waiting = refill ? s.ctl[2] : 0;
   unsigned long long c[6] = {0, 0, 0, 0, 0, 0};
   for (int e = blockIdx.x; e < count; e += gridDim.x) {
     const int64_t f = s.list[e];
@@ -807,30 +845,14 @@ __global__ void __launch_bounds__(256) stream_q_retire(const DevGraph g, ChunkSt
       c[3] += cv;
       c[4] += it;
       c[5] += cv ? it : 0;
-      const unsigned long long nf = atomicAdd(s.next, 1ull);
-      s_new = nf < static_cast<unsigned long long>(frames) ? static_cast<long long>(nf) : -1ll;
-      s.frame[f] = s_new;
-    }
-    __syncthreads();
-    const long long nf = s_new;
-    if (nf >= 0) {  // init_state (decoder.hpp:39-52) of the new frame: L only (fresh bits)
-      const float* row = llr + nf * n;
-      for (int v = threadIdx.x; v < n; v += blockDim.x)
-        s.L[static_cast<int64_t>(__ldg(g.vn_pos + v)) * s.B + f] = clamp_llr(__ldg(row + v)) * kLog2e;
-    }
-    if (threadIdx.x == 0) {
-      s.iters[f] = 0;
-      s.conv[f] = 0;
-      s.weight[f] = 0;
-      if (nf >= 0) {
-        s.done[f] = kFresh;
-      } else {
-        s.done[f] = kIdle;
-        atomicSub(s.ctl + 1, 1);
+      if (!refill) {
+        s.done[f] = kWaiting;
+        s.wlist[atomicAdd(s.ctl + 2, 1)] = static_cast<int>(f);
       }
     }
-    __syncthreads();
+    if (refill) stream_q_refill(g, s, llr, frames, f, &s_new);
   }
+  for (int e = blockIdx.x; e < waiting; e += gridDim.x) stream_q_refill(g, s, llr, frames, s.wlist[e], &s_new);
   if (threadIdx.x == 0 && a.counters)
     for (int i = 0; i < 6; ++i)
       if (c[i]) atomicAdd(a.counters + i, c[i]);
@@ -1080,6 +1102,13 @@ bool stream_queue_enabled() {
   return !e || std::atoi(e) != 0;
 }
 
+// iterations between refills of the frame queue's lanes
+int stream_refill_every() {
+  const char* e = std::getenv("LDPCB_STREAM_REFILL");
+  const int v = e ? std::atoi(e) : 4;
+  return v < 1 ? 1 : v;
+}
+
 // Early stop from a frame queue: B lanes (a multiple of 128) decode until
 // every frame of the batch has stopped. Per iteration: the groups' CN and
 // fix-up kernels, then sign words, syndrome weights, per-lane bookkeeping,
@@ -1097,7 +1126,7 @@ int launch_stream_queue(const DevGraph& g, const DecodeArgs& a, cudaStream_t st,
   s.nb = static_cast<int>(std::min<int64_t>(B, a.frames));
   s.zero_slot = g.n_slots - 1;
   const size_t state = 4ull * (static_cast<size_t>(g.n_slots) + 2ull * g.n) * B;
-  const size_t lanes = 5 * 4 * B + 8 * B + 4 * B + 64;
+  const size_t lanes = 5 * 4 * B + 8 * B + 4 * B + 4 * B + 64;
   const size_t signs = 4ull * g.n * (B / 32);
   char* mem = nullptr;
   cudaError_t err = cudaMallocAsync(reinterpret_cast<void**>(&mem), state + lanes + signs + 4 * (B / 32) + 16, st);
@@ -1112,7 +1141,8 @@ int launch_stream_queue(const DevGraph& g, const DecodeArgs& a, cudaStream_t st,
   s.berr = s.conv + B;
   s.frame = reinterpret_cast<int64_t*>(s.berr + B);
   s.list = reinterpret_cast<int*>(s.frame + B);
-  s.ctl = s.list + B;
+  s.wlist = s.list + B;
+  s.ctl = s.wlist + B;
   s.next = reinterpret_cast<unsigned long long*>(s.ctl + 8);
   s.sw = reinterpret_cast<unsigned*>(mem + state + lanes);
   // without a trace only "does any check fail" is needed per lane (stream_syndrome_or)
@@ -1147,18 +1177,25 @@ int launch_stream_queue(const DevGraph& g, const DecodeArgs& a, cudaStream_t st,
     err = cudaGetLastError();
   }
   const auto* fix4 = reinterpret_cast<const int4*>(g.fix_rec);
+  // Lanes are refilled every `every`-th iteration (LDPCB_STREAM_REFILL, default 4): only the iteration
+  // after a refill holds fresh lanes and needs the kernels with the fresh-frame code.
+  const int every = stream_refill_every();
+  bool refilled = false;  // the previous iteration ended with a refill
   for (int64_t it = 0; err == cudaSuccess; ++it) {
+    const bool fresh = refilled;
     for (int grp = 0; grp < g.G && err == cudaSuccess; ++grp) {
       const int c0 = g.h_cn_off[grp], cn = g.h_cn_off[grp + 1] - c0;
       if (cn > 0) {
-        err = launch_pdl(K.cn_fresh, blocks_for(cn * QB, tpb), tpb, st, pdl,
-                         g.cn_rec + static_cast<size_t>(c0) * g.cs, g.cs, cn, s, g.cn_fresh + c0);
+        err = launch_pdl(fresh ? K.cn_fresh : K.cn, blocks_for(cn * QB, tpb), tpb, st, pdl,
+                         g.cn_rec + static_cast<size_t>(c0) * g.cs, g.cs, cn, s,
+                         fresh ? g.cn_fresh + c0 : static_cast<const uint32_t*>(nullptr));
         ++launches;
       }
       const int x0 = g.h_fix_off[grp], xn = g.h_fix_off[grp + 1] - x0;
       if (xn > 0 && err == cudaSuccess) {
-        err = launch_pdl(K.vnsum_fresh, blocks_for(xn * QB, tpb), tpb, st, pdl,
-                         fix4 + static_cast<size_t>(x0) * g.vs4, g.vs4, xn, s, 1, g.fix_fresh + x0);
+        err = launch_pdl(fresh ? K.vnsum_fresh : K.vnsum, blocks_for(xn * QB, tpb), tpb, st, pdl,
+                         fix4 + static_cast<size_t>(x0) * g.vs4, g.vs4, xn, s, 1,
+                         fresh ? g.fix_fresh + x0 : static_cast<const uint32_t*>(nullptr));
         ++launches;
       }
     }
@@ -1171,9 +1208,12 @@ int launch_stream_queue(const DevGraph& g, const DecodeArgs& a, cudaStream_t st,
     else if (err == cudaSuccess)
       err = launch_pdl(K.syn_sw, blocks_for(g.m * QB, tpb), tpb, st, pdl, g.all_rec, g.cs, g.m, s);
     if (err == cudaSuccess)
-      err = launch_pdl(stream_q_iter_end, blocks_for(B, tpb), tpb, st, pdl, s, a.early_stop, a.trace, a.max_iters);
+      err = launch_pdl(stream_q_iter_end, blocks_for(B, tpb), tpb, st, pdl, s, a.early_stop, a.trace, a.max_iters,
+                       refilled ? 1 : 0);
+    refilled = (it + 1) % every == 0;
     if (err == cudaSuccess)
-      err = launch_pdl(stream_q_retire, static_cast<unsigned>(4 * sms), tpb, st, pdl, g, s, a, a.llr, a.frames);
+      err = launch_pdl(stream_q_retire, static_cast<unsigned>(4 * sms), tpb, st, pdl, g, s, a, a.llr, a.frames,
+                       refilled ? 1 : 0);
     launches += 4;
     const int k = static_cast<int>(it & 1);
     if (err == cudaSuccess) err = cudaMemcpyAsync(host_live + k, s.ctl + 1, sizeof(int), cudaMemcpyDeviceToHost, st);

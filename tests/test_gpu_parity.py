@@ -442,6 +442,37 @@ def test_streamed_equals_resident(P, torch, orc, case, pdl):
         os.environ.pop("LDPCB_STREAM_QUEUE", None)
 
 
+def test_stream_frame_queue_refill_interval(P, torch, orc):
+    """Lanes of the streamed frame queue are refilled every R-th iteration
+    (LDPCB_STREAM_REFILL, default 4): a stopped lane writes its outputs at
+    once and waits, so only the iteration after a refill runs the kernels
+    with the fresh-frame code. Outputs (bits, iterations, converged,
+    posteriors, traces, counters) must not depend on R."""
+    g = P.configs.c1_code()
+    s = P.configs.c1_schedules(g)["ndgsbp"]
+    F = 2500
+    llr = cu(torch, orc.transmit_batch_f32(P.sigma2_from_ebn0(1.5, g.rate), 11, g.n_vars, 0, F, THREADS))
+    os.environ["LDPCB_STREAM_CHUNK"] = "256"
+    P.set_kernel(2)
+    outs = {}
+    try:
+        for r in ("1", "2", "4", "7"):
+            os.environ["LDPCB_STREAM_REFILL"] = r
+            cnt = torch.zeros(6, dtype=torch.int64, device="cuda")
+            q = to_np(P.decode_batch(g, s, llr, 20, posterior=True, trace=True, counters=cnt))
+            outs[r] = (q, cnt.cpu().tolist())
+    finally:
+        P.set_kernel(0)
+        os.environ.pop("LDPCB_STREAM_CHUNK", None)
+        os.environ.pop("LDPCB_STREAM_REFILL", None)
+    base, cbase = outs["1"]
+    assert cbase[0] == F and 0 < cbase[3] < F  # some frames converge, some run to the limit
+    for r, (q, c) in outs.items():
+        assert c == cbase, (r, c, cbase)
+        for k in ("bits", "iterations", "converged", "posterior", "syndrome_trace"):
+            assert np.array_equal(q[k], base[k]), (r, k)
+
+
 @pytest.mark.parametrize("case", ["c1_nd", "c1_bp", "c3_nd", "irregular"])
 @pytest.mark.parametrize("lanes", ["128", "1024"])
 def test_stream_frame_queue(P, torch, orc, case, lanes):
