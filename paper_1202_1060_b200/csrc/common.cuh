@@ -216,6 +216,15 @@ __device__ __forceinline__ void boxplus_row_x2(const f32x2 (&x)[D], int deg, Sto
   emit(0, sn, sd);
 }
 
+// channel LLRs are read once: keep them out of L1, where the record tables live
+__device__ __forceinline__ float4 ldg_stream(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
 // One CN record (host.hpp KernelTables): [slot of edge 0, single-touch
 // mask, v_0 ... v_{D-1}] (v = -1 past the degree), kInts ints. Regular rows
 // of degree 3 or 6 on codes with n < 65536 use the packed 16-byte form

@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
         float4 x[U];
 #pragma unroll
         for (int u = 0; u < U; ++u)
-          if (b0 + u * nt < nv) x[u] = __ldg(l4 + b0 + u * nt);
+          if (b0 + u * nt < nv) x[u] = ldg_stream(l4 + b0 + u * nt);
 #pragma unroll
         for (int u = 0; u < U; ++u)
           if (b0 + u * nt < nv) {
@@ -790,7 +790,7 @@ __global__ void __launch_bounds__(max_threads_for(D, FV), D <= 16 ? 2 : 1) decod
       if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(a.llr) & 15) == 0) {
         const float4* l4 = reinterpret_cast<const float4*>(llr);
         for (int b = tid; b < n / 4; b += nt) {
-          const float4 x = __ldg(l4 + b);
+          const float4 x = ldg_stream(l4 + b);
           const float r[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
           for (int u = 0; u < 4; ++u) {

@@ -142,15 +142,6 @@ struct DRec {
   }
 };
 
-// channel LLRs are read once: keep them out of L1, where the record tables live
-__device__ __forceinline__ float4 ldg_stream(const float4* p) {
-  float4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "l"(p));
-  return v;
-}
-
 __device__ __forceinline__ uint32_t lo16(int w) { return static_cast<uint32_t>(w) & 0xffffu; }
 __device__ __forceinline__ uint32_t hi16(int w) { return static_cast<uint32_t>(w) >> 16; }
 

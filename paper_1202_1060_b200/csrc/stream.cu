@@ -1116,10 +1116,11 @@ int stream_refill_every() {
 // iteration behind, so the device never waits for the host.
 int launch_stream_queue(const DevGraph& g, const DecodeArgs& a, cudaStream_t st, int64_t B0) {
   const StreamKernels K = pick_v<4>(g);
-  // lanes: a quarter of the batch (so that lanes are refilled several times
-  // and the tail, where the last frames run on alone, stays short) between
-  // 2048 and 8192 (kernel efficiency); LDPCB_STREAM_CHUNK caps it
-  const int64_t want = std::min<int64_t>(std::max<int64_t>((a.frames / 4 + 127) / 128 * 128, 2048), 8192);
+  // lanes: a sixteenth of the batch (so that lanes are refilled many times
+  // and the tail, where the last frames run on alone, stays short: 8 % of a
+  // 65536-frame batch on 8192 lanes, 4 % on 4096) between 2048 and 8192
+  // (kernel efficiency); LDPCB_STREAM_CHUNK caps it
+  const int64_t want = std::min<int64_t>(std::max<int64_t>((a.frames / 16 + 127) / 128 * 128, 2048), 8192);
   const int64_t B = (std::min<int64_t>(std::min(B0, want), a.frames) + 127) / 128 * 128;
   ChunkState s;
   s.B = B;
