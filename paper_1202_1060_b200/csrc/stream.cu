@@ -773,8 +773,21 @@ __device__ __forceinline__ void stream_q_refill(const DevGraph& g, const ChunkSt
   const long long nf = *s_new;
   if (nf >= 0) {
     const float* row = llr + nf * n;
-    for (int v = threadIdx.x; v < n; v += blockDim.x)
-      s.L[static_cast<int64_t>(__ldg(g.vn_pos + v)) * s.B + f] = clamp_llr(__ldg(row + v)) * kLog2e;
+    constexpr int U = 4;  // loads of four rounds in flight before the scattered stores
+    for (int v0 = threadIdx.x; v0 < n; v0 += U * blockDim.x) {
+      int p[U];
+      float x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int v = min(v0 + u * static_cast<int>(blockDim.x), n - 1);
+        p[u] = __ldg(g.vn_pos + v);
+        x[u] = __ldg(row + v);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (v0 + u * static_cast<int>(blockDim.x) < n)
+          s.L[static_cast<int64_t>(p[u]) * s.B + f] = clamp_llr(x[u]) * kLog2e;
+    }
   }
   if (threadIdx.x == 0) {
     s.iters[f] = 0;
@@ -811,11 +824,18 @@ __global__ void __launch_bounds__(256) stream_q_retire(const DevGraph g, ChunkSt
     __syncthreads();
     int errs = 0;
     for (int b = threadIdx.x; b < nbytes; b += blockDim.x) {
+      // the eight positions, then the eight sign words, requested together (one at a time this
+      // loop was sixteen dependent L2 / DRAM latencies per byte)
+      int p[8];
+      unsigned w[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) p[j] = __ldg(g.vn_pos + min(8 * b + j, n - 1));
+#pragma unroll
+      for (int j = 0; j < 8; ++j) w[j] = __ldcg(s.sw + static_cast<int64_t>(p[j]) * (s.B / 32) + w0);
       unsigned byte = 0;
-      for (int j = 0; j < 8 && 8 * b + j < n; ++j) {
-        const int p = __ldg(g.vn_pos + 8 * b + j);
-        byte |= ((s.sw[static_cast<int64_t>(p) * (s.B / 32) + w0] >> bit) & 1u) << j;
-      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (8 * b + j < n) byte |= ((w[j] >> bit) & 1u) << j;
       if (a.bits) {
         if (a.bits_packed) {
           a.bits[fr * nbytes + b] = static_cast<uint8_t>(byte);
